@@ -1,0 +1,345 @@
+"""Benchmark of the data-parallel hot path: the wrap_optimizer gradient all-reduce.
+
+One step = one cross-replica all_reduce("premean" = all_sum(g/R))
+of a 64 MiB fp32 gradient fusion buffer per replica, in place in the registered
+pool (zero-copy), by the two-shot NVLink kernel (K2).
+
+  python bench.py                      # N=1: R=8 replicas emulated on one B200
+  torchrun --nproc-per-node N bench.py --gpus N   # N ranks, one per GPU, NVLink P2P
+  python bench.py --impl reference     # the reference's CPU path (oracle port), host cores
+
+At N=1 the 8 replicas live in one GPU's HBM and the same kernel runs as one
+cooperative launch (replica = blockIdx.y): HBM-bound. At N>1 each GPU is one replica
+and the kernel's loads/stores cross NVLink: NVLink-bound.
+
+value = n_gpus x busBW (nccl-tests busBW = 2(R-1)/R * S / t, per GPU), i.e. the
+aggregate bus bandwidth of the job. L2 is flushed (256 MiB write) between timed
+steps; every step is timed with CUDA events around the one collective launch; the
+max over ranks is reported.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+NVLINK_NOMINAL_GBS = 900.0
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--bytes", type=int, default=64 << 20, help="message bytes per replica")
+    p.add_argument("--replicas", type=int, default=8, help="replicas emulated on one GPU when N=1")
+    p.add_argument("--kind", default="premean")
+    p.add_argument("--algo", default="auto")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=10.0)
+    p.add_argument("--e2e-steps", type=int, default=10)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark(self):
+        return time.time()
+
+    def stop(self, t0, t1):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [s for (t, s) in self.samples if t0 - 0.05 <= t <= t1 + 0.1] or [s for _, s in self.samples]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+
+def peaks():
+    try:
+        d = json.load(open(MEASURED_PEAKS))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def busbw(nbytes, n, seconds):
+    return 2.0 * (n - 1) / n * nbytes / seconds / 1e9
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        return dist.get_rank(), world, local
+    return 0, 1, 0
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (oracle port), all host threads."""
+    from oracle.cpu_baseline import host_cores, time_port
+
+    n = args.replicas if world == 1 else world
+    count = args.bytes // 4
+    if rank != 0:
+        return None
+    cores = host_cores()
+    # bounded sample: whole stitched steps of the full workload for ~budget seconds
+    sec, steps, thr = time_port(n, count, args.kind, budget_s=args.cpu_budget, threads=cores,
+                                max_steps=max(1, args.steps))
+    bw = busbw(args.bytes, n, sec) * world
+    line = {
+        "metric": "all_reduce bus GB/s (aggregate, 64 MiB fp32 premean)",
+        "value": bw, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": 1,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": _config(args, world),
+        "cpu_baseline": {"value": bw, "unit": "GB/s", "cores": thr, "kind": "port",
+                         "sample": f"{steps} whole stitched steps ({n} nary_{args.kind} sites x {n} replicas x "
+                                   f"{args.bytes >> 20} MiB f32), threads={thr}"},
+        "e2e": {"value": bw, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def _config(args, world):
+    n = args.replicas if world == 1 else world
+    return {"workload": ("wrap_optimizer gradient all_reduce(premean) of one 64 MiB fp32 fusion buffer per "
+                         f"replica, {n} replicas" + (f" emulated on 1 B200 (cooperative launch)" if world == 1
+                                                      else f" on {world} B200 (one per process, NVLink P2P)")),
+            "msg_bytes_per_replica": args.bytes, "replicas": n, "dtype": "f32", "op": args.kind,
+            "algo": args.algo, "in_place_pool": True, "l2": "flushed between steps (256 MiB write)",
+            "parallelism": f"dp{n}"}
+
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    from paper_1902_00465_b200.comm import Communicator, VirtualCommunicator
+
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    count = args.bytes // 4
+    pool = args.bytes + (64 << 20)
+    if world == 1:
+        n = args.replicas
+        comm = VirtualCommunicator(n, device=local, pool_bytes=pool)
+        bufs = comm.alloc(count, torch.float32)
+        for r, b in enumerate(bufs):
+            b.copy_(torch.randn(count, device=dev, generator=torch.Generator(device=dev).manual_seed(1234 + r)))
+
+        def step():
+            comm.all_reduce(bufs, args.kind, outs=bufs, algo=args.algo)
+    else:
+        n = world
+        comm = Communicator(device=local, pool_bytes=pool)
+        buf = comm.alloc(count, torch.float32)
+        buf.copy_(torch.randn(count, device=dev, generator=torch.Generator(device=dev).manual_seed(1234 + rank)))
+
+        def step():
+            comm.all_reduce_tensor(buf, args.kind, out=buf, algo=args.algo)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    comm.check()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    barrier()
+    t_wall0 = time.time()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    barrier()
+    t_wall1 = time.time()
+    clocks = sampler.stop(t_wall0, t_wall1)
+    comm.check()
+    times = [a.elapsed_time(b) for a, b in evs]  # ms, one collective launch each
+    ms = statistics.mean(times)
+    ms = max_over_ranks(ms, world)
+    per_gpu_bus = busbw(args.bytes, n, ms / 1e3)
+    value = per_gpu_bus * world
+    hbm, hbm_src = peaks()
+    if world == 1:
+        alg_bytes = 2.0 * n * args.bytes  # every replica buffer read once, written once
+        achieved = alg_bytes / (ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
+                    "algorithmic_bytes_per_launch": alg_bytes, "kernel": "ar_twoshot<f32,premean,8>"}
+    else:
+        roofline = {"bound": "nvlink", "achieved": per_gpu_bus, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                    "frac": per_gpu_bus / NVLINK_PEER_GBS, "frac_of_nominal_900": per_gpu_bus / NVLINK_NOMINAL_GBS,
+                    "traffic": None, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
+                    "algorithmic_bytes_per_launch": 2.0 * (n - 1) / n * args.bytes,
+                    "kernel": f"ar_twoshot<f32,premean,{n}>"}
+
+    # e2e: host pinned buffers -> device -> all_reduce -> host, through the public API
+    e2e = run_e2e(args, comm, world, n, count, dev, stream)
+
+    line = {
+        "metric": "all_reduce bus GB/s (aggregate, 64 MiB fp32 premean)",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (randn, seed 1234+replica)", "config": _config(args, world),
+        "per_gpu_busbw_gbs": per_gpu_bus, "algbw_gbs": args.bytes / (ms / 1e3) / 1e9,
+        "roofline": roofline, "clocks": clocks, "e2e": e2e, "gpu_launches": args.steps,
+        "step_ms_min": min(times), "step_ms_median": statistics.median(times),
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        from oracle.cpu_baseline import time_port
+
+        sec, steps, thr = time_port(n, count, args.kind, budget_s=args.cpu_budget, threads=1, max_steps=50)
+        line["cpu_baseline"] = {"value": busbw(args.bytes, n, sec), "unit": "GB/s", "cores": thr, "kind": "port",
+                                "sample": f"{steps} whole stitched steps ({n} nary_{args.kind} sites x {n} replicas "
+                                          f"x {args.bytes >> 20} MiB f32), single-threaded numpy as the reference",
+                                "ms_per_step": sec * 1e3}
+    comm.close()
+    return line
+
+
+def run_e2e(args, comm, world, n, count, dev, stream):
+    import torch
+
+    k = max(1, args.e2e_steps)
+    reps = n if world == 1 else 1
+    host_in = [torch.randn(count).pin_memory() for _ in range(reps)]
+    host_out = torch.empty(count).pin_memory()
+    dev_in = [torch.empty(count, device=dev) for _ in range(reps)]
+
+    def step():
+        for h, d in zip(host_in, dev_in):
+            d.copy_(h, non_blocking=True)
+        if world == 1:
+            outs = comm.all_reduce(dev_in, args.kind, outs=dev_in, algo=args.algo)
+            host_out.copy_(outs[0], non_blocking=True)
+        else:
+            comm.all_reduce_tensor(dev_in[0], args.kind, out=dev_in[0], algo=args.algo)
+            host_out.copy_(dev_in[0], non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(k):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / k, world)
+    return {"value": busbw(args.bytes, n, ms / 1e3) * world, "unit": "GB/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": reps * count * 4, "d2h_bytes_per_step": count * 4,
+            "path": "pinned host -> cudaMemcpyAsync -> rp_all_reduce(_v) (staged, non-pool buffers) -> host"}
+
+
+def main():
+    args = parse()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return 0
+        line = run_reference(args, 0, world_env)
+        print(json.dumps(line), flush=True)
+        return 0
+    rank, world, local = dist_setup(args)
+    line = run_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,211 @@
+/*
+ * rp.h -- C ABI of the B200-native TF-Replicator data-parallel hot path.
+ *
+ * Plain pointers, sizes and int status codes; no torch or C++ types cross this
+ * boundary. Every collective is enqueued on the caller's CUDA stream and returns
+ * immediately (the host never blocks), which is how a Graph kernel or an
+ * optimizer wrapper calls it. One issuing host thread per communicator.
+ *
+ * Reference interfaces each entry point replaces (paths under /root/reference):
+ *   - the duck-typed communicator consumed by the mesh seam
+ *       pkg/src/replicator/graph.py:565-583 (_mesh_collective_kernel):
+ *         comm.all_reduce(local, kind in {sum,mean,max}, label)  graph.py:573-574
+ *         comm.all_gather(local, label) -> list in rank order    graph.py:575-579
+ *         comm.broadcast(root_value|None, label, shape, dtype)   graph.py:580-582
+ *   - the in-process stitched folds the MultiDevice replicator rewrites each
+ *     collective placeholder into (graph.py:506-540: nary_sum/nary_mean/nary_max,
+ *     concat/pack, pick0), served here by a *virtual* communicator whose ranks
+ *     are replicas resident on one GPU;
+ *   - the absent SPEC collectives module: ring_all_reduce / all_sum / all_reduce /
+ *     all_gather / broadcast, and the absent wrap_optimizer
+ *      and cross-replica batch norm
+ *     (PAPER.md:213-219).
+ *
+ * Status codes map one-to-one onto the reference's exception classes
+ * (pkg/src/replicator/errors.py), see RP_ERR_* below.
+ */
+#ifndef RP_H_
+#define RP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define RP_API __attribute__((visibility("default")))
+#else
+#define RP_API
+#endif
+
+typedef struct rp_comm* rp_comm_t;
+
+/* Element types. 0/1 are the reference's DTYPE_CODES (tensor.py:16-21). */
+enum {
+  RP_F32 = 0,
+  RP_F64 = 1,
+  RP_BF16 = 2,
+  RP_F16 = 3,
+};
+
+/* Reduction kinds (graph.py:514-533 and SPEC.md:406). */
+enum {
+  RP_SUM = 0,     /* nary_sum: ((x0+x1)+x2)+... ascending rank           */
+  RP_MEAN = 1,    /* nary_mean: fold_sum / N (sum, then divide)           */
+  RP_MAX = 2,     /* nary_max: np.maximum left fold                       */
+  RP_PREMEAN = 3, /* wrap_optimizer all_sum(g/R): divide, then sum        */
+};
+
+/* Algorithm selection for rp_all_reduce / rp_broadcast. */
+enum {
+  RP_ALGO_AUTO = 0,
+  RP_ALGO_ONESHOT = 1, /* every rank folds all N inputs (latency regime)      */
+  RP_ALGO_TWOSHOT = 2, /* reduce-scatter (pull) + all-gather (push)           */
+  RP_ALGO_DIRECT = 1,  /* broadcast: every rank pulls from root              */
+  RP_ALGO_SCATTER = 2, /* broadcast: scatter from root + all-gather           */
+};
+
+/* Status codes -> reference exception (errors.py). */
+enum {
+  RP_OK = 0,
+  RP_ERR_INVALID = 1,  /* bad argument / shape        -> ShapeError (errors.py:12)          */
+  RP_ERR_CONFIG = 2,   /* topology / deployment        -> ConfigurationError (errors.py:32)  */
+  RP_ERR_CUDA = 3,     /* CUDA runtime failure         -> CollectiveError (errors.py:60)     */
+  RP_ERR_ABORTED = 4,  /* a rank aborted / timed out   -> CollectiveAbortedError (errors.py:68) */
+  RP_ERR_PROTOCOL = 5, /* ranks disagree               -> ProtocolError (errors.py:64)       */
+};
+
+/* Human-readable description of the last failure on the calling thread. */
+RP_API const char* rp_last_error(void);
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Multi-process communicator: one rank per process/GPU. Allocates this rank's
+ * registered pool (pool_bytes of data + a signal region) on `device`. */
+RP_API int rp_comm_create(int rank, int world, int device, size_t pool_bytes, rp_comm_t* out);
+
+/* Virtual communicator: `world` replicas resident on ONE device (the reference's
+ * in-process MultiDevice replication, graph.py:506-540). Collectives on it take
+ * per-replica pointer arrays (the *_v entry points) and run as one cooperative
+ * kernel over all replicas' data. Usable immediately (no export/import). */
+RP_API int rp_comm_create_virtual(int world, int device, size_t pool_bytes, rp_comm_t* out);
+
+/* Size of this rank's export blob (opaque; exchanged by the caller, e.g. an
+ * all_gather over torch.distributed). */
+RP_API size_t rp_comm_export_size(void);
+RP_API int rp_comm_export(rp_comm_t comm, void* buf, size_t* len);
+
+/* `all` = world export blobs concatenated in rank order. Opens every peer's pool
+ * over CUDA IPC and checks the topology (peer access between every pair,
+ * uniform NVLink); RP_ERR_CONFIG otherwise. */
+RP_API int rp_comm_import(rp_comm_t comm, const void* all, size_t len);
+
+RP_API int rp_comm_destroy(rp_comm_t comm);
+
+/* Registered data region of replica `rank` (multi-process: only this rank;
+ * virtual: any replica). Buffers inside it are exchanged zero-copy. */
+RP_API int rp_comm_pool(rp_comm_t comm, int rank, void** base, size_t* bytes);
+
+/* Scratch window used to stage non-pool buffers: [scratch_off, pool_bytes). */
+RP_API int rp_comm_info(rp_comm_t comm, int* rank, int* world, int* is_virtual, int* num_sms,
+                 size_t* scratch_off);
+
+/* Reserve the first `bytes` of the pool for caller buffers (fusion buckets);
+ * staging uses the rest. Must be called identically on every rank. */
+RP_API int rp_comm_reserve(rp_comm_t comm, size_t bytes);
+
+/* Synchronise the device and report a collective abort/timeout recorded by the
+ * kernels (RP_ERR_ABORTED with the reason), then clear it. */
+RP_API int rp_comm_check(rp_comm_t comm);
+
+/* Spin timeout for cross-rank waits, nanoseconds (default 20 s). */
+RP_API int rp_comm_set_timeout(rp_comm_t comm, uint64_t ns);
+
+/* ---- collectives (multi-process form: this rank's buffers) ---------------- */
+
+/* dst[i] = OP over ranks of src[i], i < count. dtype_in / dtype_out are the
+ * element types of src / dst; the exchange dtype is dtype_comm (the fused cast:
+ * e.g. f32 grads exchanged as bf16 with dtype_comm=RP_BF16). Accumulation is in
+ * f32 (f32/bf16/f16) or f64 (f64), ascending rank order, rounded once.
+ * src == dst is allowed. */
+RP_API int rp_all_reduce(rp_comm_t comm, const void* src, void* dst, size_t count, int dtype_in,
+                  int dtype_comm, int dtype_out, int op, int algo, void* stream);
+
+/* dst[r*bytes_per_rank ...] = src of rank r (rank order, graph.py:575-579). */
+RP_API int rp_all_gather(rp_comm_t comm, const void* src, void* dst, size_t bytes_per_rank, void* stream);
+
+/* dst = root's src on every rank (graph.py:580-582; the reference root is 0). */
+RP_API int rp_broadcast(rp_comm_t comm, const void* src, void* dst, size_t bytes, int root, int algo,
+                 void* stream);
+
+/* ---- collectives (virtual form: one pointer per replica) ----------------- */
+
+RP_API int rp_all_reduce_v(rp_comm_t comm, const void* const* src, void* const* dst, size_t count,
+                    int dtype_in, int dtype_comm, int dtype_out, int op, int algo, void* stream);
+RP_API int rp_all_gather_v(rp_comm_t comm, const void* const* src, void* const* dst,
+                    size_t bytes_per_rank, void* stream);
+RP_API int rp_broadcast_v(rp_comm_t comm, const void* const* src, void* const* dst, size_t bytes, int root,
+                   int algo, void* stream);
+
+/* ---- cross-replica batch norm statistics --------------------------------- */
+
+/* Layouts of x / dy. */
+enum {
+  RP_LAYOUT_NC = 0,   /* [n, c]          (channels innermost)  */
+  RP_LAYOUT_NHWC = 0, /* [n, h, w, c] == [n*h*w, c]            */
+  RP_LAYOUT_NCHW = 1, /* [n, c, hw]                            */
+};
+
+/* Per-channel cross-replica statistics of x (forward, K5):
+ *   sum_c = sum over all replicas' elements of channel c, sumsq_c likewise;
+ *   mean = sum/M, var = sumsq/M - mean^2 (biased), invstd = 1/sqrt(var+eps)
+ * with M the global element count per channel (replicas may differ in batch).
+ * Local partials and the cross-replica fold are f64. Outputs (device, length c,
+ * f32): mean, var, invstd; `count` (device f64 scalar, may be NULL) receives M.
+ * `rows` = n (NCHW) or n*h*w (NHWC); `hw` = spatial size (NCHW) or 1.
+ * On a virtual communicator x/outputs are host arrays of per-replica device
+ * pointers (cast to the pointer types below). */
+RP_API int rp_bn_stats(rp_comm_t comm, const void* x, int dtype, int64_t rows, int64_t c, int64_t hw,
+                int layout, float eps, float* mean, float* var, float* invstd, double* count,
+                void* stream);
+
+/* Backward statistics (K5b): sum_dy_c and sum_dy_xmu_c = sum dy*(x-mean_c),
+ * cross-replica summed in f64, written as f32. local_sum_dy / local_sum_dy_xmu
+ * (may be NULL) receive this replica's own sums (for the weight/bias grads, which
+ * the wrapped optimizer then averages across replicas). */
+RP_API int rp_bn_bwd_stats(rp_comm_t comm, const void* x, const void* dy, int dtype, int64_t rows,
+                    int64_t c, int64_t hw, int layout, const float* mean, float* sum_dy,
+                    float* sum_dy_xmu, float* local_sum_dy, float* local_sum_dy_xmu, void* stream);
+
+/* Elementwise BN apply (forward): y = (x-mean)*invstd*w + b   (w/b may be NULL). */
+RP_API int rp_bn_apply(const void* x, void* y, int dtype, int64_t rows, int64_t c, int64_t hw, int layout,
+                const float* mean, const float* invstd, const float* weight, const float* bias,
+                void* stream);
+
+/* Elementwise BN backward: dx = (dy - sum_dy/M - (x-mean)*invstd^2*sum_dy_xmu/M)*invstd*w. */
+RP_API int rp_bn_bwd_apply(const void* x, const void* dy, void* dx, int dtype, int64_t rows, int64_t c,
+                    int64_t hw, int layout, const float* mean, const float* invstd,
+                    const float* weight, const float* sum_dy, const float* sum_dy_xmu,
+                    double count_total, void* stream);
+
+/* ---- fusion-buffer packing (K6) ------------------------------------------ */
+
+/* Gather `n` tensors (ptrs[i], counts[i] elements of dtype_src) into the flat
+ * buffer dst (dtype_dst) at element offsets offs[i], casting (RNE) on the fly;
+ * one launch for all tensors. Host arrays. */
+RP_API int rp_pack(void* dst, int dtype_dst, const void* const* ptrs, const int64_t* counts,
+            const int64_t* offs, int n, int dtype_src, void* stream);
+/* Inverse of rp_pack: scatter the flat buffer back into the tensors. */
+RP_API int rp_unpack(const void* src, int dtype_src, void* const* ptrs, const int64_t* counts,
+              const int64_t* offs, int n, int dtype_dst, void* stream);
+
+/* Library build id / version string. */
+RP_API const char* rp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RP_H_ */

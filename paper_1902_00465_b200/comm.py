@@ -1,0 +1,407 @@
+"""Communicators: the reference-facing collective seam over the sm_100a C ABI.
+
+``Communicator`` is one rank of a data-parallel group, one process per GPU. It
+implements the duck-typed interface the reference's mesh seam calls
+(``pkg/src/replicator/graph.py:565-583``)::
+
+    comm.rank
+    comm.all_reduce(local, kind in {"sum","mean","max"}, label) -> Tensor  (graph.py:573-574)
+    comm.all_gather(local, label) -> [Tensor] in rank order                (graph.py:575-579)
+    comm.broadcast(root_value | None, label, shape=..., dtype=...) -> Tensor (graph.py:580-582)
+
+accepting reference ``Tensor`` objects (anything with ``.np``), numpy arrays or torch
+tensors, and returning the same kind. Torch CUDA tensors stay on the device; host
+values are copied in and out around the kernel.
+
+``VirtualCommunicator`` holds R replicas on ONE GPU -- the reference's in-process
+MultiDevice replication, whose stitched folds are graph.py:506-540 -- and runs each
+collective as one cooperative kernel over all replicas' buffers.
+
+Bootstrap uses ``torch.distributed`` only to exchange the CUDA IPC handle blobs;
+no NCCL call sits on any collective path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+
+import numpy as np
+import torch
+
+from . import _lib, errors
+
+DEFAULT_POOL_BYTES = int(os.environ.get("RP_POOL_BYTES", str(512 << 20)))
+_ALIGN = 256
+
+_TORCH_CODE = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16,
+               torch.float16: _lib.F16}
+_NP_CODE = {np.dtype(np.float32): _lib.F32, np.dtype(np.float64): _lib.F64}
+_NAME_CODE = {"f32": _lib.F32, "f64": _lib.F64, "bf16": _lib.BF16, "f16": _lib.F16}
+_CODE_TORCH = {v: k for k, v in _TORCH_CODE.items()}
+_REF_DTYPE = {torch.float32: "f32", torch.float64: "f64"}
+
+
+def dtype_code(dt) -> int:
+    if isinstance(dt, torch.dtype):
+        code = _TORCH_CODE.get(dt)
+    elif isinstance(dt, str):
+        code = _NAME_CODE.get(dt)
+    else:
+        code = _NP_CODE.get(np.dtype(dt))
+    if code is None:
+        raise errors.ShapeError(f"unsupported element type {dt!r}; expected f32/f64/bf16/f16")
+    return code
+
+
+def _stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class _DevBuf:
+    """``__cuda_array_interface__`` view of device memory owned by a communicator."""
+
+    def __init__(self, ptr: int, nbytes: int, owner):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+        self._owner = owner
+
+
+def tensor_at(ptr: int, numel: int, dtype: torch.dtype, device: int, owner) -> torch.Tensor:
+    """A torch tensor aliasing device memory at ``ptr`` (kept alive by ``owner``)."""
+    nbytes = numel * torch.empty((), dtype=dtype).element_size()
+    raw = torch.as_tensor(_DevBuf(ptr, nbytes, owner), device=f"cuda:{device}")
+    return raw.view(dtype)
+
+
+class _Base:
+    """State shared by the multi-process and the virtual communicator."""
+
+    _handle: ctypes.c_void_p | None = None
+
+    def _init_common(self, pool_bytes: int, timeout_s: float):
+        self._lib = _lib.load()
+        self.pool_bytes = pool_bytes
+        self._reserved = 0
+        self._labels: set[str] = set()
+        self.check_labels = False
+        _lib.check(self._lib.rp_comm_set_timeout(self._handle, int(timeout_s * 1e9)), "set_timeout")
+        info = [ctypes.c_int() for _ in range(4)]
+        scratch = ctypes.c_size_t()
+        _lib.check(self._lib.rp_comm_info(self._handle, *[ctypes.byref(i) for i in info], ctypes.byref(scratch)))
+        self.num_sms = info[3].value
+
+    # -- lifecycle -----------------------------------------------------------
+    def close(self):
+        if self._handle is not None:
+            self._lib.rp_comm_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self):
+        """Synchronise and raise ``CollectiveAbortedError`` if a kernel timed out or a
+        peer aborted (include/rp.h rp_comm_check)."""
+        _lib.check(self._lib.rp_comm_check(self._handle), "collective")
+
+    def set_timeout(self, seconds: float):
+        _lib.check(self._lib.rp_comm_set_timeout(self._handle, int(seconds * 1e9)), "set_timeout")
+
+    # -- label protocol -----------------------------
+    def new_generation(self):
+        """Start a new generation (training step): labels may be reused again."""
+        self._labels.clear()
+
+    def _use_label(self, label):
+        if not self.check_labels or label is None:
+            return
+        if label in self._labels:
+            raise errors.ProtocolError(f"label {label!r} reused within one generation (SPEC.md:236)")
+        self._labels.add(label)
+
+    # -- pool ---------------------------------------------------------------
+    def _pool_ptr(self, rank: int) -> int:
+        base = ctypes.c_void_p()
+        size = ctypes.c_size_t()
+        _lib.check(self._lib.rp_comm_pool(self._handle, rank, ctypes.byref(base), ctypes.byref(size)))
+        return base.value
+
+    def _reserve(self, nbytes: int) -> int:
+        """Symmetric bump allocation in the caller part of the pool; every rank must
+        allocate the same sequence (it is SPMD code, so it does)."""
+        off = (self._reserved + _ALIGN - 1) // _ALIGN * _ALIGN
+        end = off + (nbytes + _ALIGN - 1) // _ALIGN * _ALIGN
+        _lib.check(self._lib.rp_comm_reserve(self._handle, end), "pool reserve")
+        self._reserved = end
+        return off
+
+
+class Communicator(_Base):
+    """One rank of an NVLink data-parallel group (one process per GPU).
+
+    Bootstrap over an initialised ``torch.distributed`` process group (any backend);
+    only the IPC handle blobs travel over it.
+    """
+
+    def __init__(self, group=None, device: int | None = None, pool_bytes: int = DEFAULT_POOL_BYTES,
+                 timeout_s: float = 20.0):
+        import torch.distributed as dist
+
+        lib = _lib.load()
+        if dist.is_available() and dist.is_initialized():
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            rank, world = 0, 1
+        if device is None:
+            device = torch.cuda.current_device()
+        self.rank, self.world, self.device = rank, world, int(device)
+        h = ctypes.c_void_p()
+        _lib.check(lib.rp_comm_create(rank, world, self.device, pool_bytes, ctypes.byref(h)), "comm_create")
+        self._handle = h
+        if world > 1:
+            size = lib.rp_comm_export_size()
+            buf = ctypes.create_string_buffer(size)
+            n = ctypes.c_size_t(size)
+            _lib.check(lib.rp_comm_export(h, buf, ctypes.byref(n)), "comm_export")
+            blobs = [None] * world
+            dist.all_gather_object(blobs, bytes(buf.raw[: n.value]), group=group)
+            joined = b"".join(blobs)
+            _lib.check(lib.rp_comm_import(h, joined, len(joined)), "comm_import")
+        self._init_common(pool_bytes, timeout_s)
+
+    @property
+    def num_replicas(self) -> int:
+        return self.world
+
+    # -- zero-copy buffers --------------------------------------------------
+    def alloc(self, numel: int, dtype: torch.dtype) -> torch.Tensor:
+        """Tensor inside this rank's registered pool (exchanged without staging)."""
+        esz = torch.empty((), dtype=dtype).element_size()
+        off = self._reserve(numel * esz)
+        return tensor_at(self._pool_ptr(self.rank) + off, numel, dtype, self.device, self)
+
+    # -- torch-tensor collectives ------------------------------------------
+    def _stream(self):
+        return _stream_handle(self.device)
+
+    def all_reduce_tensor(self, x: torch.Tensor, kind: str = "sum", out: torch.Tensor | None = None,
+                          comm_dtype: torch.dtype | None = None, algo: str = "auto") -> torch.Tensor:
+        """out = kind-fold of x over ranks (ascending rank order, graph.py:514-533).
+
+        kind: "sum" | "mean" (sum, then /N) | "max" | "premean" (all_sum(x/N), the
+        wrap_optimizer composition of PAPER.md:196-206). ``comm_dtype`` fuses a cast
+        (e.g. f32 tensors exchanged as bf16)."""
+        x = _contig_cuda(x, self.device)
+        if out is None:
+            out = torch.empty_like(x)
+        code = dtype_code(x.dtype)
+        ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
+        _lib.check(self._lib.rp_all_reduce(self._handle, x.data_ptr(), out.data_ptr(), x.numel(), code, ccode,
+                                           dtype_code(out.dtype), _op(kind), _algo(algo), self._stream()),
+                   "all_reduce")
+        return out
+
+    def all_gather_tensor(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """out[r] = x of rank r; out has shape (world,) + x.shape."""
+        x = _contig_cuda(x, self.device)
+        if out is None:
+            out = torch.empty((self.world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+        _lib.check(self._lib.rp_all_gather(self._handle, x.data_ptr(), out.data_ptr(),
+                                           x.numel() * x.element_size(), self._stream()), "all_gather")
+        return out
+
+    def broadcast_tensor(self, x: torch.Tensor, root: int = 0, out: torch.Tensor | None = None,
+                         algo: str = "auto") -> torch.Tensor:
+        """Every rank receives root's x (in place when out is None)."""
+        x = _contig_cuda(x, self.device)
+        if out is None:
+            out = x
+        _lib.check(self._lib.rp_broadcast(self._handle, x.data_ptr(), out.data_ptr(),
+                                          x.numel() * x.element_size(), root, _algo(algo), self._stream()),
+                   "broadcast")
+        return out
+
+    # -- the reference duck type (graph.py:565-583) -------------------------
+    def all_reduce(self, local, kind="sum", label=None, **kw):
+        self._use_label(label)
+        if isinstance(local, torch.Tensor):
+            return self.all_reduce_tensor(local, kind, **kw)
+        arr, wrap = _host_in(local)
+        x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
+        y = self.all_reduce_tensor(x, kind)
+        return wrap(y.cpu().numpy())
+
+    def all_gather(self, local, label=None):
+        self._use_label(label)
+        if isinstance(local, torch.Tensor):
+            g = self.all_gather_tensor(local)
+            return [g[r] for r in range(self.world)]
+        arr, wrap = _host_in(local)
+        x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
+        g = self.all_gather_tensor(x).cpu().numpy()
+        return [wrap(g[r]) for r in range(self.world)]
+
+    def broadcast(self, root_value, label=None, shape=None, dtype=None, root: int = 0):
+        """Reference form (graph.py:580-582): root passes its value, others pass None
+        plus ``shape``/``dtype``; every rank returns root's value bit-exactly."""
+        self._use_label(label)
+        if isinstance(root_value, torch.Tensor) or (root_value is None and isinstance(dtype, torch.dtype)):
+            x = (root_value.clone() if root_value is not None
+                 else torch.empty(tuple(shape), dtype=dtype, device=f"cuda:{self.device}"))
+            return self.broadcast_tensor(x, root)
+        if root_value is None:
+            np_dt = {"f32": np.float32, "f64": np.float64}.get(dtype, dtype)
+            arr, wrap = np.zeros(tuple(shape), dtype=np_dt), _wrapper_for(None)
+        else:
+            arr, wrap = _host_in(root_value)
+        x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
+        y = self.broadcast_tensor(x, root)
+        return wrap(y.cpu().numpy())
+
+    # -- protocol agreement (debug): every rank must issue the same collective
+    def verify(self, label: str, kind: str, shape, dtype) -> None:
+        """All ranks exchange a digest of (label, kind, shape, dtype) through this
+        communicator's own all_gather and raise ProtocolError naming the first
+        disagreeing rank."""
+        h = hashlib.sha256(repr((label, kind, tuple(shape), str(dtype))).encode()).digest()[:16]
+        t = torch.frombuffer(bytearray(h), dtype=torch.uint8).to(f"cuda:{self.device}")
+        g = self.all_gather_tensor(t).cpu()
+        for r in range(self.world):
+            if not torch.equal(g[r], g[self.rank]):
+                raise errors.ProtocolError(
+                    f"rank {r} and rank {self.rank} disagree on collective {label!r} ({kind}, {tuple(shape)})")
+
+
+class VirtualCommunicator(_Base):
+    """R replicas resident on one GPU (in-process MultiDevice replication).
+
+    Collectives take and return lists of R tensors (replica order = rank order),
+    run as one cooperative kernel; the fold is the reference's stitched
+    ``nary_*`` (graph.py:506-533), ``concat``/``pack`` (:447-449, :535-536) and
+    ``pick0`` (:538-540).
+    """
+
+    def __init__(self, num_replicas: int, device: int | None = None, pool_bytes: int = DEFAULT_POOL_BYTES,
+                 timeout_s: float = 20.0):
+        lib = _lib.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.world, self.device, self.rank = int(num_replicas), int(device), 0
+        h = ctypes.c_void_p()
+        _lib.check(lib.rp_comm_create_virtual(self.world, self.device, pool_bytes, ctypes.byref(h)),
+                   "comm_create_virtual")
+        self._handle = h
+        self._init_common(pool_bytes, timeout_s)
+
+    @property
+    def num_replicas(self) -> int:
+        return self.world
+
+    def alloc(self, numel: int, dtype: torch.dtype) -> list[torch.Tensor]:
+        esz = torch.empty((), dtype=dtype).element_size()
+        off = self._reserve(numel * esz)
+        return [tensor_at(self._pool_ptr(r) + off, numel, dtype, self.device, self) for r in range(self.world)]
+
+    def _check_list(self, xs):
+        if len(xs) != self.world:
+            raise errors.ShapeError(f"expected {self.world} replica tensors, got {len(xs)}")
+        xs = [_contig_cuda(x, self.device) for x in xs]
+        s0, d0 = xs[0].shape, xs[0].dtype
+        for r, x in enumerate(xs):
+            if x.shape != s0 or x.dtype != d0:
+                raise errors.ProtocolError(f"replica {r} disagrees: {tuple(x.shape)}/{x.dtype} vs {tuple(s0)}/{d0}")
+        return xs
+
+    def all_reduce(self, xs, kind="sum", outs=None, comm_dtype=None, algo="auto", label=None):
+        self._use_label(label)
+        xs = self._check_list(xs)
+        if outs is None:
+            outs = [torch.empty_like(x) for x in xs]
+        code = dtype_code(xs[0].dtype)
+        ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
+        sp, _k1 = _lib.ptr_array([x.data_ptr() for x in xs])
+        dp, _k2 = _lib.ptr_array([o.data_ptr() for o in outs])
+        _lib.check(self._lib.rp_all_reduce_v(self._handle, sp, dp, xs[0].numel(), code, ccode,
+                                             dtype_code(outs[0].dtype), _op(kind), _algo(algo),
+                                             _stream_handle(self.device)), "all_reduce")
+        return outs
+
+    def all_gather(self, xs, outs=None, label=None):
+        """outs[r] has shape (R,) + x.shape: every replica's x in rank order."""
+        self._use_label(label)
+        xs = self._check_list(xs)
+        if outs is None:
+            outs = [torch.empty((self.world,) + tuple(xs[0].shape), dtype=xs[0].dtype, device=xs[0].device)
+                    for _ in xs]
+        sp, _k1 = _lib.ptr_array([x.data_ptr() for x in xs])
+        dp, _k2 = _lib.ptr_array([o.data_ptr() for o in outs])
+        _lib.check(self._lib.rp_all_gather_v(self._handle, sp, dp, xs[0].numel() * xs[0].element_size(),
+                                             _stream_handle(self.device)), "all_gather")
+        return outs
+
+    def broadcast(self, xs, root=0, outs=None, algo="auto", label=None):
+        self._use_label(label)
+        xs = self._check_list(xs)
+        if outs is None:
+            outs = [torch.empty_like(x) for x in xs]
+        sp, _k1 = _lib.ptr_array([x.data_ptr() for x in xs])
+        dp, _k2 = _lib.ptr_array([o.data_ptr() for o in outs])
+        _lib.check(self._lib.rp_broadcast_v(self._handle, sp, dp, xs[0].numel() * xs[0].element_size(), root,
+                                            _algo(algo), _stream_handle(self.device)), "broadcast")
+        return outs
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def _op(kind: str) -> int:
+    try:
+        return _lib.OPS[kind]
+    except KeyError:
+        raise errors.ShapeError(f"unknown reduction kind {kind!r}; expected sum/mean/max/premean") from None
+
+
+def _algo(algo) -> int:
+    if isinstance(algo, int):
+        return algo
+    try:
+        return _lib.ALGOS[algo]
+    except KeyError:
+        raise errors.ShapeError(f"unknown algorithm {algo!r}") from None
+
+
+def _contig_cuda(x: torch.Tensor, device: int) -> torch.Tensor:
+    if not x.is_cuda:
+        raise errors.ShapeError("collective inputs must be CUDA tensors (host values go through the "
+                                "reference seam methods, which copy them in)")
+    if x.device.index != device:
+        raise errors.ShapeError(f"tensor on cuda:{x.device.index}, communicator on cuda:{device}")
+    return x if x.is_contiguous() else x.contiguous()
+
+
+def _wrapper_for(local):
+    """Return a function turning a numpy result back into the caller's value kind:
+    the reference Tensor class when given one (``Tensor.wrap``, tensor.py:52-62),
+    else a numpy array."""
+    if local is not None and hasattr(local, "np") and hasattr(type(local), "wrap"):
+        cls = type(local)
+
+        def wrap(a):
+            a = np.ascontiguousarray(a)
+            a.setflags(write=False)
+            return cls.wrap(a)
+        return wrap
+    return lambda a: np.ascontiguousarray(a)
+
+
+def _host_in(local):
+    arr = local.np if hasattr(local, "np") else np.asarray(local)
+    if arr.dtype not in (np.float32, np.float64):
+        raise errors.ShapeError(f"unsupported element type {arr.dtype}; only f32/f64 tensors exist")
+    return arr, _wrapper_for(local)

@@ -1,0 +1,558 @@
+// Cross-replica batch-norm statistics (K5 forward, K5b backward) and the
+// elementwise BN apply kernels.
+//
+// Reference: the cross-replica BN listing PAPER.md:213-219 (mean = all_sum(mean/R),
+// mean_sq = all_sum(mean(h^2)/R)) with SPEC.md:530's corrected variance
+// E[h^2]-E[h]^2 and eps=1e-5 inside the sqrt, generalised to per-channel
+// statistics. The reference cannot differentiate through its collectives
+// (graph.py:562, :585); K5b supplies the backward reduction.
+//
+// Two launches per statistics call:
+//   bn_partial_*  : HBM-bound local pass. Every thread accumulates its channels
+//                   in f64 over a slice of rows and the block folds its rows in a
+//                   fixed order -> per-split partials P[split][c] (sum, sumsq).
+//   bn_exchange   : one thread per channel folds P over splits (fixed order),
+//                   publishes (sum, sumsq, count) in its pool's BN records,
+//                   meets its peers on a BN signal row, folds all ranks' records
+//                   in ascending rank order (f64) and writes the outputs.
+#include <algorithm>
+
+#include "rp_device.cuh"
+
+namespace rp {
+
+constexpr int kBnThreads = 256;
+constexpr int kExThreads = 256;
+
+struct BnArgs {
+  const void* x[RP_MAX_RANKS];
+  const void* dy[RP_MAX_RANKS];
+  const float* mean[RP_MAX_RANKS];
+  double* part[RP_MAX_RANKS];  // per local replica: [S][C][2]
+  int64_t rows, C, hw;
+  int S;
+};
+
+struct ExArgs {
+  RankTable t;
+  double* part[RP_MAX_RANKS];
+  float* out0[RP_MAX_RANKS];
+  float* out1[RP_MAX_RANKS];
+  float* out2[RP_MAX_RANKS];
+  float* out3[RP_MAX_RANKS];
+  double* count[RP_MAX_RANKS];
+  size_t bn_off;  // pool offset of the BN records
+  int64_t C;
+  double local_count[RP_MAX_RANKS];
+  int S;
+  int world;
+  int rank;  // -1: virtual (rank = blockIdx.y)
+  int bwd;
+  float eps;
+  uint32_t epoch;
+  uint64_t timeout_ns;
+};
+
+template <typename T>
+__device__ __forceinline__ double ld_as_f64(const T* p) {
+  return (double)to_acc(*p);
+}
+
+// f64 block reduction of NV values per thread over threadIdx.y (fixed order).
+template <int NV>
+__device__ __forceinline__ void reduce_rows_y(double (&v)[NV], double* smem) {
+  // smem: [blockDim.y][blockDim.x][NV]
+  const int tx = threadIdx.x, ty = threadIdx.y, bx = blockDim.x;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) smem[(ty * bx + tx) * NV + k] = v[k];
+  __syncthreads();
+  if (ty == 0) {
+    for (int y = 1; y < (int)blockDim.y; ++y)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[k] += smem[(y * bx + tx) * NV + k];
+  }
+}
+
+// --- NHWC / NC: x is [rows, C], channels innermost ---------------------------
+// block (32, 8): threadIdx.x -> VEC consecutive channels, threadIdx.y -> rows.
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
+  constexpr int VEC = 16 / sizeof(T);
+  extern __shared__ double smem[];
+  const int rep = blockIdx.z;
+  const T* x = (const T*)a.x[rep];
+  const T* dy = BWD ? (const T*)a.dy[rep] : nullptr;
+  const int64_t C = a.C, M = a.rows;
+  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  const int64_t rps = (M + a.S - 1) / a.S;
+  const int64_t r0 = (int64_t)blockIdx.y * rps, r1 = std::min(r0 + rps, M);
+  double s1[VEC], s2[VEC], mu[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) {
+    s1[k] = 0.0;
+    s2[k] = 0.0;
+    mu[k] = (BWD && c0 + k < C) ? (double)a.mean[rep][c0 + k] : 0.0;
+  }
+  const bool full = c0 + VEC <= C;
+  const bool vec = full && (C % VEC == 0) && ((((uintptr_t)x) & 15u) == 0) &&
+                   (!BWD || ((((uintptr_t)dy) & 15u) == 0));
+  if (c0 < C) {
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
+      const int64_t base = r * C + c0;
+      if (vec) {
+        Pack16<T> px;
+        px.u = ld128_stream(x + base);
+        if (BWD) {
+          Pack16<T> pd;
+          pd.u = ld128_stream(dy + base);
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            const double d = (double)to_acc(pd.e[k]);
+            s1[k] += d;
+            s2[k] = fma(d, (double)to_acc(px.e[k]) - mu[k], s2[k]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            const double v = (double)to_acc(px.e[k]);
+            s1[k] += v;
+            s2[k] = fma(v, v, s2[k]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          if (c0 + k >= C) break;
+          const double v = ld_as_f64(x + base + k);
+          if (BWD) {
+            const double d = ld_as_f64(dy + base + k);
+            s1[k] += d;
+            s2[k] = fma(d, v - mu[k], s2[k]);
+          } else {
+            s1[k] += v;
+            s2[k] = fma(v, v, s2[k]);
+          }
+        }
+      }
+    }
+  }
+  double v[2 * VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) {
+    v[2 * k] = s1[k];
+    v[2 * k + 1] = s2[k];
+  }
+  reduce_rows_y<2 * VEC>(v, smem);
+  if (threadIdx.y == 0 && c0 < C) {
+    double* P = a.part[rep] + ((int64_t)blockIdx.y * C) * 2;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k)
+      if (c0 + k < C) {
+        P[(c0 + k) * 2] = v[2 * k];
+        P[(c0 + k) * 2 + 1] = v[2 * k + 1];
+      }
+  }
+}
+
+// --- NCHW: x is [n, C, hw] ---------------------------------------------------
+// block (c, split): 8 warps take samples round-robin, lanes stride the hw plane.
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(kBnThreads) bn_partial_nchw(const BnArgs a) {
+  constexpr int VEC = 16 / sizeof(T);
+  __shared__ double red[kBnThreads / 32][2];
+  const int rep = blockIdx.z;
+  const T* x = (const T*)a.x[rep];
+  const T* dy = BWD ? (const T*)a.dy[rep] : nullptr;
+  const int64_t C = a.C, N = a.rows, HW = a.hw;
+  const int64_t c = blockIdx.x;
+  const int64_t nps = (N + a.S - 1) / a.S;
+  const int64_t n0 = (int64_t)blockIdx.y * nps, n1 = std::min(n0 + nps, N);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const double mu = BWD ? (double)a.mean[rep][c] : 0.0;
+  const bool vec = (HW % VEC == 0) && ((((uintptr_t)x) & 15u) == 0) &&
+                   (!BWD || ((((uintptr_t)dy) & 15u) == 0));
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t n = n0 + warp; n < n1; n += nwarps) {
+    const int64_t base = (n * C + c) * HW;
+    if (vec) {
+      for (int64_t j = (int64_t)lane * VEC; j < HW; j += 32 * VEC) {
+        Pack16<T> px;
+        px.u = ld128_stream(x + base + j);
+        if (BWD) {
+          Pack16<T> pd;
+          pd.u = ld128_stream(dy + base + j);
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            const double d = (double)to_acc(pd.e[k]);
+            s1 += d;
+            s2 = fma(d, (double)to_acc(px.e[k]) - mu, s2);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            const double v = (double)to_acc(px.e[k]);
+            s1 += v;
+            s2 = fma(v, v, s2);
+          }
+        }
+      }
+    } else {
+      for (int64_t j = lane; j < HW; j += 32) {
+        const double v = ld_as_f64(x + base + j);
+        if (BWD) {
+          const double d = ld_as_f64(dy + base + j);
+          s1 += d;
+          s2 = fma(d, v - mu, s2);
+        } else {
+          s1 += v;
+          s2 = fma(v, v, s2);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_down_sync(0xffffffffu, s1, o);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    red[warp][0] = s1;
+    red[warp][1] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nwarps; ++w) {
+      s1 += red[w][0];
+      s2 += red[w][1];
+    }
+    double* P = a.part[rep] + ((int64_t)blockIdx.y * C + c) * 2;
+    P[0] = s1;
+    P[1] = s2;
+  }
+}
+
+// --- exchange: fold splits, publish, fold ranks ------------------------------
+__global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
+  const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  const int rep = a.rank >= 0 ? 0 : rank;  // local replica index
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t C = a.C;
+  if (c < C) {
+    const double* P = a.part[rep];
+    double s1 = 0.0, s2 = 0.0;
+    for (int s = 0; s < a.S; ++s) {
+      s1 += P[((int64_t)s * C + c) * 2];
+      s2 += P[((int64_t)s * C + c) * 2 + 1];
+    }
+    if (a.bwd) {  // this replica's own sums (weight / bias gradients)
+      if (a.out2[rep]) a.out2[rep][c] = (float)s1;
+      if (a.out3[rep]) a.out3[rep][c] = (float)s2;
+    }
+    double* rec = (double*)(a.t.data[rank] + a.bn_off) + c * 3;
+    rec[0] = s1;
+    rec[1] = s2;
+    rec[2] = a.local_count[rep];
+  }
+  if (!rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, a.epoch + 1)) return;
+  if (c < C) {
+    double A1 = 0.0, A2 = 0.0, Mt = 0.0;
+    for (int p = 0; p < a.world; ++p) {  // ascending rank order
+      const double* rec = (const double*)(a.t.data[p] + a.bn_off) + c * 3;
+      A1 += rec[0];
+      A2 += rec[1];
+      Mt += rec[2];
+    }
+    if (a.bwd) {
+      a.out0[rep][c] = (float)A1;
+      a.out1[rep][c] = (float)A2;
+    } else {
+      const double mean = A1 / Mt;
+      double var = A2 / Mt - mean * mean;
+      var = var < 0.0 ? 0.0 : var;
+      a.out0[rep][c] = (float)mean;
+      a.out1[rep][c] = (float)var;
+      a.out2[rep][c] = (float)(1.0 / sqrt(var + (double)a.eps));
+    }
+    if (c == 0 && a.count[rep]) *a.count[rep] = Mt;
+  }
+  rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, a.epoch + 2);
+}
+
+// --- elementwise apply ----------------------------------------------------------
+// chan(i) for element i: NHWC -> i % C ; NCHW -> (i / hw) % C
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(kBnThreads) bn_apply_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                                              T* __restrict__ y, int64_t total, int64_t C,
+                                                              int64_t hw, int nchw, const float* __restrict__ mean,
+                                                              const float* __restrict__ invstd,
+                                                              const float* __restrict__ w, const float* __restrict__ b,
+                                                              const float* __restrict__ sum_dy,
+                                                              const float* __restrict__ sum_dy_xmu, float inv_m) {
+  constexpr int VEC = 16 / sizeof(T);
+  const bool vec = (((((uintptr_t)x) | ((uintptr_t)y) | (BWD ? (uintptr_t)dy : 0)) & 15u) == 0) &&
+                   (nchw ? (hw % VEC == 0) : (C % VEC == 0));
+  auto coef = [&](int64_t ch, float& m, float& s, float& k1, float& k2) {
+    m = mean[ch];
+    s = invstd[ch];
+    const float g = w ? w[ch] : 1.0f;
+    if (BWD) {
+      k1 = sum_dy[ch] * inv_m;
+      k2 = s * s * sum_dy_xmu[ch] * inv_m;
+      s = s * g;  // final multiplier
+    } else {
+      k1 = s * g;                 // scale
+      k2 = b ? b[ch] : 0.0f;      // shift
+    }
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    const int64_t nv = total / VEC;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+      const int64_t i0 = v * VEC;
+      Pack16<T> px, pd, py;
+      px.u = ld128_stream(x + i0);
+      if (BWD) pd.u = ld128_stream(dy + i0);
+      if (nchw) {
+        float m, s, k1, k2;
+        coef((i0 / hw) % C, m, s, k1, k2);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          const float xv = to_acc(px.e[k]);
+          float r;
+          if (BWD) r = (to_acc(pd.e[k]) - k1 - (xv - m) * k2) * s;
+          else r = (xv - m) * k1 + k2;
+          py.e[k] = from_f32<T>(r);
+        }
+      } else {
+        const int64_t c0 = i0 % C;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          float m, s, k1, k2;
+          coef(c0 + k, m, s, k1, k2);
+          const float xv = to_acc(px.e[k]);
+          float r;
+          if (BWD) r = (to_acc(pd.e[k]) - k1 - (xv - m) * k2) * s;
+          else r = (xv - m) * k1 + k2;
+          py.e[k] = from_f32<T>(r);
+        }
+      }
+      st128(y + i0, py.u);
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int64_t ch = nchw ? (i / hw) % C : i % C;
+      float m, s, k1, k2;
+      coef(ch, m, s, k1, k2);
+      const float xv = to_acc(x[i]);
+      float r;
+      if (BWD) r = (to_acc(dy[i]) - k1 - (xv - m) * k2) * s;
+      else r = (xv - m) * k1 + k2;
+      y[i] = from_f32<T>(r);
+    }
+  }
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+namespace {
+
+int ensure_partials(rp_comm* c, size_t bytes) {
+  if (bytes <= c->bn_partials_bytes) return RP_OK;
+  if (c->bn_partials) {
+    cudaDeviceSynchronize();
+    cudaFree(c->bn_partials);
+    c->bn_partials = nullptr;
+    c->bn_partials_bytes = 0;
+  }
+  RP_CUDA_CHECK(cudaMalloc(&c->bn_partials, bytes));
+  c->bn_partials_bytes = bytes;
+  return RP_OK;
+}
+
+template <bool BWD>
+const void* pick_partial(int dtype, int layout) {
+  const bool nchw = layout == RP_LAYOUT_NCHW;
+#define RP_B(DT, T) \
+  if (dtype == DT) return nchw ? (const void*)bn_partial_nchw<T, BWD> : (const void*)bn_partial_nhwc<T, BWD>;
+  RP_B(RP_F32, float)
+  RP_B(RP_BF16, __nv_bfloat16)
+  RP_B(RP_F16, __half)
+  RP_B(RP_F64, double)
+#undef RP_B
+  return nullptr;
+}
+
+int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, int64_t rows, int64_t ch, int64_t hw,
+              int layout, float eps, const float* mean, float* o0, float* o1, float* o2, float* o3, double* count,
+              cudaStream_t stream) {
+  if (ch <= 0 || rows < 0 || hw <= 0) return rp_fail(RP_ERR_INVALID, "bn: bad shape");
+  if (ch > (int64_t)RP_BN_ROWS * kExThreads) return rp_fail(RP_ERR_INVALID, "bn: too many channels (max 65536)");
+  if (layout != RP_LAYOUT_NHWC && layout != RP_LAYOUT_NCHW) return rp_fail(RP_ERR_INVALID, "bn: unknown layout");
+  if (layout == RP_LAYOUT_NHWC && hw != 1) return rp_fail(RP_ERR_INVALID, "bn: NHWC/NC layout takes hw == 1");
+  const void* fn = bwd ? pick_partial<true>(dtype, layout) : pick_partial<false>(dtype, layout);
+  if (!fn) return rp_fail(RP_ERR_INVALID, "bn: unsupported dtype");
+  const int W = c->world;
+  const int nrep = c->is_virtual ? W : 1;
+  const size_t esz = rp_dtype_size(dtype);
+  const int vec = (int)(16 / esz);
+
+  BnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.rows = rows;
+  a.C = ch;
+  a.hw = hw;
+  // pointer plumbing: virtual communicators pass host arrays of per-replica pointers
+  for (int i = 0; i < nrep; ++i) {
+    a.x[i] = c->is_virtual ? ((const void* const*)x)[i] : x;
+    if (bwd) {
+      a.dy[i] = c->is_virtual ? ((const void* const*)dy)[i] : dy;
+      a.mean[i] = c->is_virtual ? ((const float* const*)mean)[i] : mean;
+    }
+  }
+  dim3 grid, block;
+  size_t smem = 0;
+  const int target = 4 * c->num_sms;
+  if (layout == RP_LAYOUT_NHWC) {
+    block = dim3(32, kBnThreads / 32);
+    const int cb = (int)((ch + 32LL * vec - 1) / (32LL * vec));
+    int S = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, (target + cb - 1) / cb));
+    a.S = S;
+    grid = dim3(cb, S, nrep);
+    smem = (size_t)kBnThreads * 2 * vec * sizeof(double);
+  } else {
+    block = dim3(kBnThreads);
+    int S = (int)std::max<int64_t>(1, std::min<int64_t>(rows, (target + ch - 1) / ch));
+    S = std::min(S, 65535);
+    a.S = S;
+    grid = dim3((unsigned)ch, S, nrep);
+  }
+  const size_t per_rep = (size_t)a.S * ch * 2 * sizeof(double);
+  int rc = ensure_partials(c, per_rep * nrep);
+  if (rc) return rc;
+  for (int i = 0; i < nrep; ++i) a.part[i] = c->bn_partials + (per_rep / sizeof(double)) * i;
+  if (smem > 48 * 1024) {
+    RP_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  if (rows > 0) {
+    void* args[] = {&a};
+    RP_CUDA_CHECK(cudaLaunchKernel(fn, grid, block, args, smem, stream));
+  } else {
+    RP_CUDA_CHECK(cudaMemsetAsync(c->bn_partials, 0, per_rep * nrep, stream));
+  }
+
+  ExArgs e;
+  memset(&e, 0, sizeof(e));
+  e.t = c->table;
+  e.bn_off = c->scratch_end();
+  e.C = ch;
+  e.S = a.S;
+  e.world = W;
+  e.rank = c->is_virtual ? -1 : c->rank;
+  e.bwd = bwd ? 1 : 0;
+  e.eps = eps;
+  e.timeout_ns = c->timeout_ns;
+  for (int i = 0; i < nrep; ++i) {
+    e.part[i] = a.part[i];
+    e.local_count[i] = (double)rows * (double)hw;
+    if (c->is_virtual) {
+      e.out0[i] = ((float* const*)o0)[i];
+      e.out1[i] = ((float* const*)o1)[i];
+      e.out2[i] = o2 ? ((float* const*)o2)[i] : nullptr;
+      e.out3[i] = o3 ? ((float* const*)o3)[i] : nullptr;
+      e.count[i] = count ? ((double* const*)count)[i] : nullptr;
+    } else {
+      e.out0[i] = o0;
+      e.out1[i] = o1;
+      e.out2[i] = o2;
+      e.out3[i] = o3;
+      e.count[i] = count;
+    }
+  }
+  const int blocks = (int)((ch + kExThreads - 1) / kExThreads);
+  e.epoch = c->epoch;
+  c->epoch += 2;
+  void* args[] = {&e};
+  return rp_launch(c, (const void*)bn_exchange, dim3(blocks, c->is_virtual ? W : 1), dim3(kExThreads), args, 0,
+                   stream);
+}
+
+}  // namespace
+
+int rp_launch_bn_stats(rp_comm* c, const void* x, int dtype, int64_t rows, int64_t ch, int64_t hw, int layout,
+                       float eps, float* mean, float* var, float* invstd, double* count, cudaStream_t stream) {
+  if (!mean || !var || !invstd) return rp_fail(RP_ERR_INVALID, "bn_stats: NULL output");
+  return bn_common(c, false, x, nullptr, dtype, rows, ch, hw, layout, eps, nullptr, mean, var, invstd, nullptr,
+                   count, stream);
+}
+
+int rp_launch_bn_bwd_stats(rp_comm* c, const void* x, const void* dy, int dtype, int64_t rows, int64_t ch,
+                           int64_t hw, int layout, const float* mean, float* sum_dy, float* sum_dy_xmu,
+                           float* local_sum_dy, float* local_sum_dy_xmu, cudaStream_t stream) {
+  if (!mean || !sum_dy || !sum_dy_xmu) return rp_fail(RP_ERR_INVALID, "bn_bwd_stats: NULL argument");
+  return bn_common(c, true, x, dy, dtype, rows, ch, hw, layout, 0.0f, mean, sum_dy, sum_dy_xmu, local_sum_dy,
+                   local_sum_dy_xmu, nullptr, stream);
+}
+
+extern "C" {
+
+int rp_bn_apply(const void* x, void* y, int dtype, int64_t rows, int64_t ch, int64_t hw, int layout,
+                const float* mean, const float* invstd, const float* weight, const float* bias, void* stream) {
+  const int64_t total = rows * ch * hw;
+  if (total == 0) return RP_OK;
+  const int nchw = layout == RP_LAYOUT_NCHW;
+  const float* none = nullptr;
+  const void* fn = nullptr;
+  switch (dtype) {
+    case RP_F32: fn = (const void*)bn_apply_kernel<float, false>; break;
+    case RP_BF16: fn = (const void*)bn_apply_kernel<__nv_bfloat16, false>; break;
+    case RP_F16: fn = (const void*)bn_apply_kernel<__half, false>; break;
+    default: return rp_fail(RP_ERR_INVALID, "bn_apply: dtype must be f32/bf16/f16");
+  }
+  const void* dy = nullptr;
+  float inv_m = 0.0f;
+  int64_t C = ch, HW = hw;
+  void* args[] = {(void*)&x, (void*)&dy, (void*)&y, (void*)&total, (void*)&C, (void*)&HW, (void*)&nchw,
+                  (void*)&mean, (void*)&invstd, (void*)&weight, (void*)&bias, (void*)&none, (void*)&none,
+                  (void*)&inv_m};
+  int rc = rp_set_device_from_ptr(x);
+  if (rc) return rc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = (int)std::min<int64_t>((total / 8 + kBnThreads - 1) / kBnThreads + 1, (int64_t)sms * 8);
+  RP_CUDA_CHECK(cudaLaunchKernel(fn, dim3(blocks), dim3(kBnThreads), args, 0, (cudaStream_t)stream));
+  return RP_OK;
+}
+
+int rp_bn_bwd_apply(const void* x, const void* dy, void* dx, int dtype, int64_t rows, int64_t ch, int64_t hw,
+                    int layout, const float* mean, const float* invstd, const float* weight, const float* sum_dy,
+                    const float* sum_dy_xmu, double count_total, void* stream) {
+  const int64_t total = rows * ch * hw;
+  if (total == 0) return RP_OK;
+  const int nchw = layout == RP_LAYOUT_NCHW;
+  const float* none = nullptr;
+  const void* fn = nullptr;
+  switch (dtype) {
+    case RP_F32: fn = (const void*)bn_apply_kernel<float, true>; break;
+    case RP_BF16: fn = (const void*)bn_apply_kernel<__nv_bfloat16, true>; break;
+    case RP_F16: fn = (const void*)bn_apply_kernel<__half, true>; break;
+    default: return rp_fail(RP_ERR_INVALID, "bn_bwd_apply: dtype must be f32/bf16/f16");
+  }
+  float inv_m = (float)(1.0 / count_total);
+  int64_t C = ch, HW = hw;
+  void* args[] = {(void*)&x, (void*)&dy, (void*)&dx, (void*)&total, (void*)&C, (void*)&HW, (void*)&nchw,
+                  (void*)&mean, (void*)&invstd, (void*)&weight, (void*)&none, (void*)&sum_dy, (void*)&sum_dy_xmu,
+                  (void*)&inv_m};
+  int rc = rp_set_device_from_ptr(x);
+  if (rc) return rc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = (int)std::min<int64_t>((total / 8 + kBnThreads - 1) / kBnThreads + 1, (int64_t)sms * 8);
+  RP_CUDA_CHECK(cudaLaunchKernel(fn, dim3(blocks), dim3(kBnThreads), args, 0, (cudaStream_t)stream));
+  return RP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,441 @@
+// Cross-replica collectives over NVLink/NVSwitch peer memory (sm_100a).
+//
+//   K1 ar_oneshot  : every rank folds all N inputs (ascending rank) for its block's
+//                    slice and writes the result locally. Latency regime.
+//   K2 ar_twoshot  : reduce-scatter by pulling chunk `rank` from every peer, fold in
+//                    rank order, push the rounded result into every peer's buffer
+//                    (all-gather by stores). In-place safe: the only reader of
+//                    chunk r of any buffer is rank r itself, before it writes it.
+//   K3 allgather   : pull every peer's slot into dst in rank order.
+//   K4 broadcast   : direct pull from root, or scatter from root + all-gather.
+//
+// Every kernel partitions work so that block b of rank r depends only on block
+// b of its peers; one signal row per block index carries the barrier (see
+// rp_device.cuh). Replaces the reference's in-process folds (graph.py:506-540),
+// the mesh seam's communicator calls (graph.py:565-583) and the SPEC ring
+// (SPEC.md:188-222).
+#include <algorithm>
+
+#include "rp_device.cuh"
+
+const void* rp_pick_ar_f32(int op, int algo, int world);
+const void* rp_pick_ar_f64(int op, int algo, int world);
+const void* rp_pick_ar_bf16(int op, int algo, int world);
+const void* rp_pick_ar_f16(int op, int algo, int world);
+
+static const void* pick_ar_any(int dtype, int op, int algo, int world) {
+  switch (dtype) {
+    case RP_F32: return rp_pick_ar_f32(op, algo, world);
+    case RP_F64: return rp_pick_ar_f64(op, algo, world);
+    case RP_BF16: return rp_pick_ar_bf16(op, algo, world);
+    case RP_F16: return rp_pick_ar_f16(op, algo, world);
+  }
+  return nullptr;
+}
+
+namespace rp {
+
+constexpr int kThreads = 512;
+
+__device__ __forceinline__ bool aligned16(const void* p) { return (((uintptr_t)p) & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+// byte copies (all_gather / broadcast)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void copy_bytes(char* dst, const char* src, size_t lo, size_t hi, bool vec) {
+  if (vec) {  // lo, hi multiples of 16, pointers 16-aligned
+    const size_t step = (size_t)blockDim.x * 16 * 4;
+    for (size_t o = lo + threadIdx.x * 16; o < hi; o += step) {
+      uint4 r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t oo = o + (size_t)u * blockDim.x * 16;
+        if (oo < hi) r[u] = ld128(src + oo);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t oo = o + (size_t)u * blockDim.x * 16;
+        if (oo < hi) st128(dst + oo, r[u]);
+      }
+    }
+  } else {
+    for (size_t o = lo + threadIdx.x; o < hi; o += blockDim.x) dst[o] = src[o];
+  }
+}
+
+// K3: all_gather. Rank p's contribution lives at pool_p[read_off + p*read_stride].
+// a.count = bytes per rank, a.chunk = per-block byte slice (multiple of 16).
+__global__ void __launch_bounds__(kThreads) allgather_kernel(const CollArgs a, size_t read_stride, int vec) {
+  const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  const size_t B = a.count;
+  const size_t lo = (size_t)blockIdx.x * a.chunk;
+  const size_t hi = std::min(lo + a.chunk, B);
+  if (a.copy_in && lo < hi)
+    copy_bytes(a.t.data[rank] + a.read_off + rank * read_stride, (const char*)a.src[rank], lo, hi, vec);
+  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  char* dst = (char*)a.dst[rank];
+  if (lo < hi) {
+    for (int i = 0; i < a.world; ++i) {
+      const int p = (rank + i) % a.world;  // stagger peers to spread NVLink load
+      const char* src = a.t.data[p] + a.read_off + p * read_stride;
+      char* d = dst + (size_t)p * B;
+      if (d == src) continue;  // in-place slot already holds our data
+      copy_bytes(d, src, lo, hi, vec);
+    }
+  }
+  rank_barrier(a, rank, blockIdx.x, a.epoch + 2);
+}
+
+// K4a: direct broadcast: every rank pulls root's pool copy.
+__global__ void __launch_bounds__(kThreads) bcast_direct_kernel(const CollArgs a, int vec) {
+  const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  const size_t B = a.count;
+  const size_t lo = (size_t)blockIdx.x * a.chunk;
+  const size_t hi = std::min(lo + a.chunk, B);
+  if (rank == a.root && a.copy_in && lo < hi)
+    copy_bytes(a.t.data[rank] + a.read_off, (const char*)a.src[rank], lo, hi, vec);
+  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  const char* src = a.t.data[a.root] + a.read_off;
+  char* dst = (char*)a.dst[rank];
+  if (lo < hi && dst != src) copy_bytes(dst, src, lo, hi, vec);
+  rank_barrier(a, rank, blockIdx.x, a.epoch + 2);
+}
+
+// K4b: scatter + all-gather broadcast. The message is cut into `world` chunks
+// of a.chunk*gridDim.x bytes... precisely: chunk c = [c*C, (c+1)*C), C = per-rank
+// bytes (multiple of 16*gridDim.x); block b owns slice b of every chunk.
+__global__ void __launch_bounds__(kThreads) bcast_scatter_kernel(const CollArgs a, size_t C, int vec) {
+  const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  const size_t B = a.count;
+  const size_t s0 = (size_t)blockIdx.x * a.chunk;
+  const size_t s1 = std::min(s0 + a.chunk, C);
+  char* root_pool = a.t.data[a.root] + a.read_off;
+  if (rank == a.root && a.copy_in && s0 < s1) {
+    for (int c = 0; c < a.world; ++c) {
+      const size_t lo = c * C + s0, hi = std::min(c * C + s1, B);
+      if (lo < hi) copy_bytes(root_pool, (const char*)a.src[rank], lo, hi, vec);
+    }
+  }
+  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  // scatter: pull my chunk from root into my pool staging (root keeps its own)
+  char* my_stage = a.t.data[rank] + a.write_off;
+  {
+    const size_t lo = rank * C + s0, hi = std::min(rank * C + s1, B);
+    if (lo < hi && rank != a.root) copy_bytes(my_stage, root_pool, lo, hi, vec);
+  }
+  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 2)) return;
+  // all-gather: pull chunk c from its owner's staging (root's chunks from root_pool)
+  char* dst = (char*)a.dst[rank];
+  for (int i = 0; i < a.world; ++i) {
+    const int c = (rank + i) % a.world;
+    const size_t lo = c * C + s0, hi = std::min(c * C + s1, B);
+    if (lo >= hi) continue;
+    const char* src = (c == a.root) ? root_pool : (a.t.data[c] + a.write_off);
+    if (dst + 0 == src) continue;
+    copy_bytes(dst, src, lo, hi, vec);
+  }
+  rank_barrier(a, rank, blockIdx.x, a.epoch + 3);
+}
+
+}  // namespace rp
+
+// ===========================================================================
+// host launchers
+// ===========================================================================
+using namespace rp;
+
+namespace {
+
+// Find which pool offset (if any) a pointer of rank r lies in.
+bool in_pool(rp_comm* c, int r, const void* p, size_t bytes, size_t* off) {
+  const char* base = c->table.data[r];
+  const char* q = (const char*)p;
+  if (q >= base && q + bytes <= base + c->pool_bytes) {
+    *off = (size_t)(q - base);
+    return true;
+  }
+  return false;
+}
+
+// Every replica's pointer at the same pool offset (symmetric allocation).
+bool symmetric_in_pool(rp_comm* c, const void* const* ptrs, size_t bytes, size_t* off) {
+  const int n = c->is_virtual ? c->world : 1;
+  size_t o0 = 0;
+  for (int i = 0; i < n; ++i) {
+    const int r = c->is_virtual ? i : c->rank;
+    size_t o;
+    if (!in_pool(c, r, ptrs[i], bytes, &o)) return false;
+    if (i == 0) o0 = o;
+    else if (o != o0) return false;
+  }
+  *off = o0;
+  return true;
+}
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+void fill_ptrs(rp_comm* c, CollArgs& a, const void* const* src, void* const* dst) {
+  const int n = c->is_virtual ? c->world : 1;
+  for (int i = 0; i < RP_MAX_RANKS; ++i) {
+    a.src[i] = nullptr;
+    a.dst[i] = nullptr;
+  }
+  for (int i = 0; i < n; ++i) {
+    const int r = c->is_virtual ? i : c->rank;
+    a.src[r] = src ? src[i] : nullptr;
+    a.dst[r] = dst ? dst[i] : nullptr;
+  }
+}
+
+void base_args(rp_comm* c, CollArgs& a) {
+  a.t = c->table;
+  a.world = c->world;
+  a.rank = c->is_virtual ? -1 : c->rank;
+  a.timeout_ns = c->timeout_ns;
+  a.epoch = c->epoch;
+}
+
+}  // namespace
+
+int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, size_t count,
+                         int dtype_in, int dtype_comm, int dtype_out, int op, int algo,
+                         cudaStream_t stream) {
+  if (count == 0) return RP_OK;
+  if (!rp_dtype_valid(dtype_in) || !rp_dtype_valid(dtype_comm) || !rp_dtype_valid(dtype_out))
+    return rp_fail(RP_ERR_INVALID, "all_reduce: unknown dtype");
+  if (op < RP_SUM || op > RP_PREMEAN) return rp_fail(RP_ERR_INVALID, "all_reduce: unknown op");
+  auto pair_ok = [&](int user) {
+    return user == dtype_comm ||
+           (user == RP_F32 && (dtype_comm == RP_BF16 || dtype_comm == RP_F16));
+  };
+  if (!pair_ok(dtype_in) || !pair_ok(dtype_out))
+    return rp_fail(RP_ERR_INVALID, "all_reduce: dtype_in/dtype_out must equal dtype_comm "
+                                   "or be f32 with a 16-bit dtype_comm");
+  const size_t esz = rp_dtype_size(dtype_comm);
+  const size_t vec = 16 / esz;
+  const size_t V = (count + vec - 1) / vec;
+  const int W = c->world;
+  const int nrep = c->is_virtual ? W : 1;
+
+  CollArgs a;
+  base_args(c, a);
+  fill_ptrs(c, a, src, dst);
+  a.count = count;
+  a.dtype_in = dtype_in;
+  a.dtype_out = dtype_out;
+  a.root = 0;
+  a.chunk = 0;
+  a.read_off = a.write_off = 0;
+  a.copy_in = a.copy_out = 0;
+
+  if (W == 1) {  // a single replica: the fold of one operand (identity / x/1)
+    const void* fn = pick_ar_any(dtype_comm, op, RP_ALGO_TWOSHOT, 1);
+    a.src[0] = src[0];
+    a.dst[0] = dst[0];
+    const int blocks = (int)std::min<size_t>((V + kThreads - 1) / kThreads, (size_t)c->num_sms * 4);
+    void* args[] = {&a};
+    RP_CUDA_CHECK(cudaLaunchKernel(fn, dim3(std::max(blocks, 1)), dim3(kThreads), args, 0, stream));
+    return RP_OK;
+  }
+
+  // Algorithm: deterministic in (bytes, world), hence identical on every rank.
+  const size_t bytes = count * esz;
+  if (algo == RP_ALGO_AUTO) {
+    const size_t oneshot_max = W <= 2 ? ((size_t)512 << 10) : (W <= 4 ? ((size_t)256 << 10) : ((size_t)128 << 10));
+    algo = bytes <= oneshot_max ? RP_ALGO_ONESHOT : RP_ALGO_TWOSHOT;
+  }
+  if (algo != RP_ALGO_ONESHOT && algo != RP_ALGO_TWOSHOT)
+    return rp_fail(RP_ERR_INVALID, "all_reduce: unknown algorithm");
+
+  // Placement. Pool-resident buffers (symmetric offsets, allocated identically on
+  // every rank) are exchanged zero-copy; anything else is staged through scratch.
+  const size_t padded = round_up(V * 16, RP_ALIGN);
+  size_t src_off = 0, dst_off = 0;
+  const bool src_pool = dtype_in == dtype_comm &&
+                        symmetric_in_pool(c, src, count * rp_dtype_size(dtype_in), &src_off);
+  const bool dst_pool = dtype_out == dtype_comm &&
+                        symmetric_in_pool(c, (const void* const*)dst, count * rp_dtype_size(dtype_out), &dst_off);
+  if (src_pool && dst_pool && src_off != dst_off &&
+      !(dst_off + padded <= src_off || src_off + padded <= dst_off))
+    return rp_fail(RP_ERR_INVALID, "all_reduce: partially overlapping pool buffers");
+  if (algo == RP_ALGO_ONESHOT && src_pool && dst_pool && src_off == dst_off)
+    algo = RP_ALGO_TWOSHOT;  // in-place: peers are still reading our input
+
+  const size_t scratch = round_up(c->reserved, RP_ALIGN);
+  const size_t scratch_end = c->scratch_end();
+  size_t need_scratch = 0;
+  if (algo == RP_ALGO_ONESHOT) {
+    a.copy_in = !src_pool;
+    a.read_off = src_pool ? src_off : scratch;
+    a.copy_out = 1;  // every rank writes its own dst directly (with the output cast)
+    need_scratch = src_pool ? 0 : padded;
+  } else if (src_pool && dst_pool) {
+    a.read_off = src_off;
+    a.write_off = dst_off;
+  } else if (src_pool) {          // keep src intact: push into scratch, copy out
+    a.read_off = src_off;
+    a.write_off = scratch;
+    a.copy_out = 1;
+    need_scratch = padded;
+  } else if (dst_pool) {          // stage in, push straight into the dst region
+    a.copy_in = 1;
+    a.read_off = scratch;
+    a.write_off = dst_off;
+    need_scratch = padded;
+  } else {                        // stage in, reduce in place in scratch, copy out
+    a.copy_in = 1;
+    a.copy_out = 1;
+    a.read_off = a.write_off = scratch;
+    need_scratch = padded;
+  }
+
+  if (scratch + need_scratch > scratch_end) {
+    // Stage in pieces that fit the scratch window (each piece is a full collective).
+    const size_t avail = scratch_end > scratch ? scratch_end - scratch : 0;
+    size_t piece = (avail / 16) * vec;
+    piece -= piece % ((size_t)W * vec * 64);
+    if (piece == 0) return rp_fail(RP_ERR_INVALID, "all_reduce: pool too small to stage the message");
+    for (size_t off = 0; off < count; off += piece) {
+      const size_t n = std::min(piece, count - off);
+      const void* s2[RP_MAX_RANKS];
+      void* d2[RP_MAX_RANKS];
+      for (int i = 0; i < nrep; ++i) {
+        s2[i] = (const char*)src[i] + off * rp_dtype_size(dtype_in);
+        d2[i] = (char*)dst[i] + off * rp_dtype_size(dtype_out);
+      }
+      const int rc = rp_launch_all_reduce(c, s2, d2, n, dtype_in, dtype_comm, dtype_out, op, algo, stream);
+      if (rc) return rc;
+    }
+    return RP_OK;
+  }
+
+  const void* fn = pick_ar_any(dtype_comm, op, algo, W);
+  if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
+
+  size_t work;  // vectors one rank's blocks cover
+  if (algo == RP_ALGO_TWOSHOT) {
+    a.chunk = (V + W - 1) / W;
+    work = a.chunk;
+  } else {
+    work = V;
+  }
+  const size_t per_block = (size_t)kThreads * 2;
+  int blocks = (int)std::min<size_t>((work + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
+  blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
+  a.epoch = c->epoch;
+  c->epoch += 2;
+  void* args[] = {&a};
+  return rp_launch(c, fn, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads), args, 0, stream);
+}
+
+// All-gather: rank order (graph.py:575-579). Inputs are read from the peers'
+// pools: in place (src == dst + rank*bytes, dst in the pool) or staged.
+int rp_launch_all_gather(rp_comm* c, const void* const* src, void* const* dst, size_t bytes,
+                         cudaStream_t stream) {
+  if (bytes == 0) return RP_OK;
+  const int W = c->world;
+  const int nrep = c->is_virtual ? W : 1;
+  CollArgs a;
+  base_args(c, a);
+  fill_ptrs(c, a, src, dst);
+  a.count = bytes;
+  a.copy_out = 0;
+  a.write_off = 0;
+  a.root = 0;
+  bool vec = (bytes % 16) == 0;
+  for (int i = 0; i < nrep; ++i)
+    vec = vec && ((uintptr_t)src[i] % 16 == 0) && ((uintptr_t)dst[i] % 16 == 0);
+  const size_t scratch = round_up(c->reserved, RP_ALIGN);
+  const size_t scratch_end = c->scratch_end();
+  bool in_place = true;
+  for (int i = 0; i < nrep && in_place; ++i) {
+    const int r = c->is_virtual ? i : c->rank;
+    in_place = (const char*)src[i] == (const char*)dst[i] + (size_t)r * bytes;
+  }
+  size_t read_stride = 0, doff = 0;
+  if (in_place && symmetric_in_pool(c, (const void* const*)dst, bytes * W, &doff)) {
+    a.copy_in = 0;
+    a.read_off = doff;
+    read_stride = bytes;
+  } else {
+    if (scratch + round_up(bytes, RP_ALIGN) > scratch_end)
+      return rp_fail(RP_ERR_INVALID, "all_gather: per-rank message exceeds the staging pool");
+    a.copy_in = 1;
+    a.read_off = scratch;
+  }
+  const size_t per_block_min = (size_t)16 * kThreads * 4;
+  const int want = (int)std::min<size_t>((bytes + per_block_min - 1) / per_block_min, (size_t)RP_MAX_BLOCKS);
+  const int blocks = rp_blocks_per_rank(c, (const void*)allgather_kernel, kThreads, std::max(want, 1));
+  a.chunk = round_up((bytes + blocks - 1) / blocks, 16);
+  int ivec = vec ? 1 : 0;
+  a.epoch = c->epoch;
+  c->epoch += 2;
+  void* args[] = {&a, &read_stride, &ivec};
+  return rp_launch(c, (const void*)allgather_kernel, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads),
+                   args, 0, stream);
+}
+
+// Broadcast from `root` (the reference always uses rank 0, graph.py:581).
+// In place (src == dst on every rank, dst in the pool) the root's buffer is read
+// directly; otherwise the root stages its src into scratch.
+int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, size_t bytes, int root,
+                        int algo, cudaStream_t stream) {
+  if (bytes == 0) return RP_OK;
+  const int W = c->world;
+  if (root < 0 || root >= W) return rp_fail(RP_ERR_INVALID, "broadcast: root out of range");
+  const int nrep = c->is_virtual ? W : 1;
+  CollArgs a;
+  base_args(c, a);
+  fill_ptrs(c, a, src, dst);
+  a.count = bytes;
+  a.root = root;
+  a.copy_out = 0;
+  const size_t scratch = round_up(c->reserved, RP_ALIGN);
+  const size_t scratch_end = c->scratch_end();
+  const size_t pb = round_up(bytes, RP_ALIGN);
+  bool vec = (bytes % 16) == 0;
+  bool in_place = true;
+  for (int i = 0; i < nrep; ++i) {
+    const int r = c->is_virtual ? i : c->rank;
+    if (r == root) vec = vec && ((uintptr_t)src[i] % 16 == 0);
+    vec = vec && ((uintptr_t)dst[i] % 16 == 0);
+    in_place = in_place && (src[i] == dst[i]);
+  }
+  size_t doff = 0;
+  if (in_place && symmetric_in_pool(c, (const void* const*)dst, bytes, &doff)) {
+    a.copy_in = 0;
+    a.read_off = doff;
+  } else {
+    a.copy_in = 1;
+    a.read_off = scratch;
+  }
+  if (algo == RP_ALGO_AUTO) algo = (bytes >= ((size_t)1 << 20) && W > 2) ? RP_ALGO_SCATTER : RP_ALGO_DIRECT;
+  if (algo == RP_ALGO_SCATTER) {
+    a.write_off = a.copy_in ? scratch + pb : scratch;  // per-rank staging of its chunk
+    if (a.write_off + pb > scratch_end) algo = RP_ALGO_DIRECT;
+  }
+  if (a.copy_in && scratch + pb > scratch_end)
+    return rp_fail(RP_ERR_INVALID, "broadcast: message exceeds the staging pool");
+  int ivec = vec ? 1 : 0;
+  const size_t per_block_min = (size_t)16 * kThreads * 4;
+  a.epoch = c->epoch;
+  if (algo == RP_ALGO_SCATTER) {
+    const int want = (int)std::min<size_t>((bytes / W + per_block_min - 1) / per_block_min, (size_t)RP_MAX_BLOCKS);
+    const int blocks = rp_blocks_per_rank(c, (const void*)bcast_scatter_kernel, kThreads, std::max(want, 1));
+    size_t C = round_up((bytes + W - 1) / W, (size_t)16 * blocks);
+    a.chunk = C / blocks;
+    c->epoch += 3;
+    void* args[] = {&a, &C, &ivec};
+    return rp_launch(c, (const void*)bcast_scatter_kernel, dim3(blocks, c->is_virtual ? W : 1),
+                     dim3(kThreads), args, 0, stream);
+  }
+  a.write_off = 0;
+  const int want = (int)std::min<size_t>((bytes + per_block_min - 1) / per_block_min, (size_t)RP_MAX_BLOCKS);
+  const int blocks = rp_blocks_per_rank(c, (const void*)bcast_direct_kernel, kThreads, std::max(want, 1));
+  a.chunk = round_up((bytes + blocks - 1) / blocks, 16);
+  c->epoch += 2;
+  void* args[] = {&a, &ivec};
+  return rp_launch(c, (const void*)bcast_direct_kernel, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads),
+                   args, 0, stream);
+}

@@ -1,0 +1,505 @@
+// Communicator lifecycle, topology discovery, the exported C ABI (include/rp.h)
+// and the K6 fusion-buffer pack/unpack kernels.
+//
+// Bootstrap: each rank allocates one device region [signals | data pool], exports
+// a CUDA IPC handle, and the caller exchanges the blobs (torch.distributed over
+// NCCL/gloo, used ONLY for this). rp_comm_import maps every peer's region into
+// this process, so kernels address peers' pools as plain device pointers that
+// resolve over NVLink/NVSwitch. Replaces the reference's transport layer
+// and its communicator (graph.py:565-583).
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+
+#include "rp_device.cuh"
+
+static thread_local std::string g_last_error;
+
+void rp_set_error(const std::string& msg) { g_last_error = msg; }
+int rp_fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+size_t rp_dtype_size(int dtype) {
+  switch (dtype) {
+    case RP_F32: return 4;
+    case RP_F64: return 8;
+    case RP_BF16: return 2;
+    case RP_F16: return 2;
+  }
+  return 0;
+}
+bool rp_dtype_valid(int dtype) { return rp_dtype_size(dtype) != 0; }
+
+int rp_set_device_from_ptr(const void* p) {
+  cudaPointerAttributes at;
+  RP_CUDA_CHECK(cudaPointerGetAttributes(&at, p));
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return rp_fail(RP_ERR_INVALID, "expected a device pointer");
+  RP_CUDA_CHECK(cudaSetDevice(at.device));
+  return RP_OK;
+}
+
+static const uint64_t kMagic = 0x52505f434f4d4d31ull;  // "RP_COMM1"
+
+int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+  // Every block of every (virtual) rank must be co-resident: blocks wait on
+  // their peers' blocks of the same index.
+  int cap = occ * c->num_sms;
+  if (c->is_virtual) cap /= c->world;
+  cap = std::min(cap, RP_MAX_BLOCKS);
+  return std::max(1, std::min(want, cap));
+}
+
+int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, size_t smem,
+              cudaStream_t stream) {
+  cudaError_t e;
+  if (c->is_virtual && c->world > 1)
+    e = cudaLaunchCooperativeKernel(func, grid, block, args, smem, stream);
+  else
+    e = cudaLaunchKernel(func, grid, block, args, smem, stream);
+  if (e != cudaSuccess) return rp_fail(RP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return RP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K6: multi-tensor pack / unpack with fused cast (one launch per <=96 tensors)
+// ---------------------------------------------------------------------------
+namespace rp {
+
+constexpr int kPackMax = 96;
+constexpr int kPackThreads = 256;
+constexpr int kPackElemsPerBlock = 8192;
+
+struct PackTable {
+  const void* ptr[kPackMax];  // tensor data (src for pack, dst for unpack)
+  int64_t count[kPackMax];
+  int64_t off[kPackMax];      // element offset in the flat buffer
+  int32_t block0[kPackMax + 1];
+  int n;
+};
+
+template <typename S, typename D>
+__device__ __forceinline__ void copy_cast(D* dst, const S* src, int64_t n) {
+  // 8 elements per step; vector path when both sides are 16-byte aligned
+  const bool al = ((((uintptr_t)dst) | ((uintptr_t)src)) & 15u) == 0;
+  int64_t i = 0;
+  if (al) {
+    const int64_t nv = n / 8;
+    for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      S s[8];
+      D d[8];
+      if constexpr (sizeof(S) == 2) {
+        *(uint4*)s = ld128_stream(src + v * 8);
+      } else if constexpr (sizeof(S) == 4) {
+        *(uint4*)s = ld128_stream(src + v * 8);
+        *(uint4*)(s + 4) = ld128_stream(src + v * 8 + 4);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) *(uint4*)(s + 2 * k) = ld128_stream(src + v * 8 + 2 * k);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) d[k] = convert<D>(s[k]);
+      if constexpr (sizeof(D) == 2) {
+        st128(dst + v * 8, *(uint4*)d);
+      } else if constexpr (sizeof(D) == 4) {
+        st128(dst + v * 8, *(uint4*)d);
+        st128(dst + v * 8 + 4, *(uint4*)(d + 4));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st128(dst + v * 8 + 2 * k, *(uint4*)(d + 2 * k));
+      }
+    }
+    i = nv * 8;
+  }
+  for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) dst[j] = convert<D>(src[j]);
+}
+
+template <typename S, typename D, bool PACK>
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(const PackTable t, void* flat) {
+  // locate this block's tensor (block0 is a prefix sum of blocks per tensor)
+  int lo = 0, hi = t.n - 1;
+  const int b = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.block0[mid] <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  const int i = lo;
+  const int64_t start = (int64_t)(b - t.block0[i]) * kPackElemsPerBlock;
+  const int64_t n = std::min<int64_t>(kPackElemsPerBlock, t.count[i] - start);
+  if (n <= 0) return;
+  if (PACK) {
+    copy_cast<S, D>((D*)flat + t.off[i] + start, (const S*)t.ptr[i] + start, n);
+  } else {
+    copy_cast<S, D>((D*)t.ptr[i] + start, (const S*)flat + t.off[i] + start, n);
+  }
+}
+
+template <bool PACK>
+const void* pick_pack(int s, int d) {
+#define RP_P(SD, ST, DD, DT) \
+  if (s == SD && d == DD) return (const void*)pack_kernel<ST, DT, PACK>;
+  RP_P(RP_F32, float, RP_F32, float)
+  RP_P(RP_F32, float, RP_BF16, __nv_bfloat16)
+  RP_P(RP_F32, float, RP_F16, __half)
+  RP_P(RP_BF16, __nv_bfloat16, RP_F32, float)
+  RP_P(RP_F16, __half, RP_F32, float)
+  RP_P(RP_BF16, __nv_bfloat16, RP_BF16, __nv_bfloat16)
+  RP_P(RP_F16, __half, RP_F16, __half)
+  RP_P(RP_F64, double, RP_F64, double)
+#undef RP_P
+  return nullptr;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+static int pack_common(bool pack, void* flat, int dtype_flat, const void* const* ptrs, const int64_t* counts,
+                       const int64_t* offs, int n, int dtype_t, cudaStream_t stream) {
+  const void* fn = pack ? pick_pack<true>(dtype_t, dtype_flat) : pick_pack<false>(dtype_flat, dtype_t);
+  if (!fn) return rp_fail(RP_ERR_INVALID, "pack/unpack: unsupported dtype pair");
+  if (n <= 0) return RP_OK;
+  int rc = rp_set_device_from_ptr(flat);
+  if (rc) return rc;
+  for (int base = 0; base < n; base += kPackMax) {
+    PackTable t;
+    memset(&t, 0, sizeof(t));
+    t.n = std::min(kPackMax, n - base);
+    int blocks = 0;
+    for (int i = 0; i < t.n; ++i) {
+      t.ptr[i] = ptrs[base + i];
+      t.count[i] = counts[base + i];
+      t.off[i] = offs[base + i];
+      t.block0[i] = blocks;
+      blocks += (int)((counts[base + i] + kPackElemsPerBlock - 1) / kPackElemsPerBlock);
+    }
+    t.block0[t.n] = blocks;
+    if (blocks == 0) continue;
+    void* args[] = {&t, &flat};
+    cudaError_t e = cudaLaunchKernel(fn, dim3(blocks), dim3(kPackThreads), args, 0, stream);
+    if (e != cudaSuccess) return rp_fail(RP_ERR_CUDA, std::string("pack launch: ") + cudaGetErrorString(e));
+  }
+  return RP_OK;
+}
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* rp_last_error(void) { return g_last_error.c_str(); }
+
+const char* rp_version(void) { return "rp 0.1.0 sm_100a"; }
+
+static int init_device(rp_comm* c) {
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  cudaDeviceProp prop;
+  RP_CUDA_CHECK(cudaGetDeviceProperties(&prop, c->device));
+  c->num_sms = prop.multiProcessorCount;
+  if (prop.major < 10)
+    return rp_fail(RP_ERR_CONFIG, "device " + std::to_string(c->device) + " (" + prop.name +
+                                      ") is not sm_100-class; this library is built for sm_100a only");
+  return RP_OK;
+}
+
+static int alloc_region(rp_comm* c, int r) {
+  char* base = nullptr;
+  RP_CUDA_CHECK(cudaMalloc(&base, RP_SIGNAL_BYTES + c->pool_bytes));
+  RP_CUDA_CHECK(cudaMemset(base, 0, RP_SIGNAL_BYTES));
+  c->alloc[r] = base;
+  c->table.sig[r] = (uint32_t*)base;
+  c->table.data[r] = base + RP_SIGNAL_BYTES;
+  return RP_OK;
+}
+
+int rp_comm_create(int rank, int world, int device, size_t pool_bytes, rp_comm_t* out) {
+  if (!out) return rp_fail(RP_ERR_INVALID, "rp_comm_create: out is NULL");
+  if (world < 1 || world > RP_MAX_RANKS || rank < 0 || rank >= world)
+    return rp_fail(RP_ERR_CONFIG, "rp_comm_create: need 1 <= world <= 8 and 0 <= rank < world");
+  if (pool_bytes < RP_MIN_POOL) return rp_fail(RP_ERR_INVALID, "rp_comm_create: pool_bytes must be >= 4 MiB");
+  rp_comm* c = new rp_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->pool_bytes = (pool_bytes + RP_ALIGN - 1) / RP_ALIGN * RP_ALIGN;
+  int rc = init_device(c);
+  if (!rc) rc = alloc_region(c, rank);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  if (world == 1) c->imported = true;
+  *out = c;
+  return RP_OK;
+}
+
+int rp_comm_create_virtual(int world, int device, size_t pool_bytes, rp_comm_t* out) {
+  if (!out) return rp_fail(RP_ERR_INVALID, "rp_comm_create_virtual: out is NULL");
+  if (world < 1 || world > RP_MAX_RANKS) return rp_fail(RP_ERR_CONFIG, "virtual world must be 1..8");
+  if (pool_bytes < RP_MIN_POOL) return rp_fail(RP_ERR_INVALID, "rp_comm_create_virtual: pool_bytes must be >= 4 MiB");
+  rp_comm* c = new rp_comm();
+  c->world = world;
+  c->device = device;
+  c->is_virtual = true;
+  c->pool_bytes = (pool_bytes + RP_ALIGN - 1) / RP_ALIGN * RP_ALIGN;
+  int rc = init_device(c);
+  for (int r = 0; r < world && !rc; ++r) rc = alloc_region(c, r);
+  if (!rc && world > 1) {
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    if (!coop) rc = rp_fail(RP_ERR_CONFIG, "device lacks cooperative launch (needed by virtual replicas)");
+  }
+  if (rc) {
+    for (int r = 0; r < world; ++r)
+      if (c->alloc[r]) cudaFree(c->alloc[r]);
+    delete c;
+    return rc;
+  }
+  c->imported = true;
+  *out = c;
+  return RP_OK;
+}
+
+size_t rp_comm_export_size(void) { return sizeof(RpExport); }
+
+int rp_comm_export(rp_comm_t c, void* buf, size_t* len) {
+  if (!c || !buf || !len) return rp_fail(RP_ERR_INVALID, "rp_comm_export: NULL argument");
+  if (c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_comm_export: virtual communicators need no export");
+  if (*len < sizeof(RpExport)) return rp_fail(RP_ERR_INVALID, "rp_comm_export: buffer too small");
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  RpExport e;
+  memset(&e, 0, sizeof(e));
+  e.magic = kMagic;
+  e.rank = c->rank;
+  e.world = c->world;
+  e.pool_bytes = c->pool_bytes;
+  RP_CUDA_CHECK(cudaIpcGetMemHandle(&e.handle, c->alloc[c->rank]));
+  cudaDeviceProp prop;
+  RP_CUDA_CHECK(cudaGetDeviceProperties(&prop, c->device));
+  memcpy(e.uuid, &prop.uuid, 16);
+  e.pci_bus = prop.pciBusID;
+  e.pci_device = prop.pciDeviceID;
+  e.pci_domain = prop.pciDomainID;
+  memcpy(buf, &e, sizeof(e));
+  *len = sizeof(e);
+  return RP_OK;
+}
+
+int rp_comm_import(rp_comm_t c, const void* all, size_t len) {
+  if (!c || !all) return rp_fail(RP_ERR_INVALID, "rp_comm_import: NULL argument");
+  if (c->is_virtual || c->world == 1) return RP_OK;
+  if (len != sizeof(RpExport) * (size_t)c->world)
+    return rp_fail(RP_ERR_PROTOCOL, "rp_comm_import: expected world export blobs");
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  const RpExport* ex = (const RpExport*)all;
+  // topology: map peer UUIDs to local ordinals (when visible) and require P2P
+  int ndev = 0;
+  RP_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+  for (int p = 0; p < c->world; ++p) {
+    if (ex[p].magic != kMagic || ex[p].rank != p || ex[p].world != c->world)
+      return rp_fail(RP_ERR_PROTOCOL, "rp_comm_import: blob " + std::to_string(p) + " is not rank " +
+                                          std::to_string(p) + " of this world");
+    if (ex[p].pool_bytes != c->pool_bytes)
+      return rp_fail(RP_ERR_PROTOCOL, "rp_comm_import: ranks disagree on pool_bytes");
+    if (p == c->rank) continue;
+    if (memcmp(ex[p].uuid, ex[c->rank].uuid, 16) == 0)
+      return rp_fail(RP_ERR_CONFIG, "ranks " + std::to_string(c->rank) + " and " + std::to_string(p) +
+                                        " share one GPU; use a virtual communicator for replicas on one device");
+    for (int d = 0; d < ndev; ++d) {
+      cudaDeviceProp prop;
+      if (cudaGetDeviceProperties(&prop, d) != cudaSuccess) continue;
+      if (memcmp(&prop.uuid, ex[p].uuid, 16) != 0) continue;
+      int ok = 0;
+      RP_CUDA_CHECK(cudaDeviceCanAccessPeer(&ok, c->device, d));
+      int acc = 0;
+      cudaDeviceGetP2PAttribute(&acc, cudaDevP2PAttrAccessSupported, c->device, d);
+      if (!ok || !acc)
+        return rp_fail(RP_ERR_CONFIG, "no peer access between device " + std::to_string(c->device) +
+                                          " and device " + std::to_string(d) +
+                                          " (NVLink/NVSwitch all-to-all required; no fallback)");
+    }
+  }
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) continue;
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, ex[p].handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return rp_fail(RP_ERR_CONFIG, "cudaIpcOpenMemHandle(rank " + std::to_string(p) + "): " + cudaGetErrorString(e));
+    c->ipc_opened[p] = true;
+    c->alloc[p] = (char*)ptr;
+    c->table.sig[p] = (uint32_t*)ptr;
+    c->table.data[p] = (char*)ptr + RP_SIGNAL_BYTES;
+  }
+  c->imported = true;
+  return RP_OK;
+}
+
+int rp_comm_destroy(rp_comm_t c) {
+  if (!c) return RP_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < RP_MAX_RANKS; ++r) {
+    if (!c->alloc[r]) continue;
+    if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->alloc[r]);
+    else cudaFree(c->alloc[r]);
+  }
+  if (c->bn_partials) cudaFree(c->bn_partials);
+  delete c;
+  return RP_OK;
+}
+
+int rp_comm_pool(rp_comm_t c, int rank, void** base, size_t* bytes) {
+  if (!c || !base || !bytes) return rp_fail(RP_ERR_INVALID, "rp_comm_pool: NULL argument");
+  const int r = rank < 0 ? c->rank : rank;
+  if (r < 0 || r >= c->world || (!c->is_virtual && r != c->rank))
+    return rp_fail(RP_ERR_INVALID, "rp_comm_pool: rank not local to this process");
+  *base = c->table.data[r];
+  *bytes = c->pool_bytes;
+  return RP_OK;
+}
+
+int rp_comm_info(rp_comm_t c, int* rank, int* world, int* is_virtual, int* num_sms, size_t* scratch_off) {
+  if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_info: NULL comm");
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (is_virtual) *is_virtual = c->is_virtual ? 1 : 0;
+  if (num_sms) *num_sms = c->num_sms;
+  if (scratch_off) *scratch_off = (c->reserved + RP_ALIGN - 1) / RP_ALIGN * RP_ALIGN;
+  return RP_OK;
+}
+
+int rp_comm_reserve(rp_comm_t c, size_t bytes) {
+  if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_reserve: NULL comm");
+  if (bytes > c->scratch_end()) return rp_fail(RP_ERR_INVALID, "rp_comm_reserve: exceeds pool");
+  c->reserved = bytes;
+  return RP_OK;
+}
+
+int rp_comm_set_timeout(rp_comm_t c, uint64_t ns) {
+  if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_set_timeout: NULL comm");
+  c->timeout_ns = ns;
+  return RP_OK;
+}
+
+int rp_comm_check(rp_comm_t c) {
+  if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_check: NULL comm");
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  RP_CUDA_CHECK(cudaDeviceSynchronize());
+  uint32_t worst = 0;
+  for (int r = 0; r < c->world; ++r) {
+    if (!c->is_virtual && r != c->rank) continue;
+    uint32_t w = 0;
+    RP_CUDA_CHECK(cudaMemcpy(&w, c->table.sig[r] + RP_ABORT_WORD, 4, cudaMemcpyDeviceToHost));
+    worst = std::max(worst, w);
+  }
+  if (worst == RP_ABORT_TIMEOUT)
+    return rp_fail(RP_ERR_ABORTED, "collective timed out waiting for a peer (dead or diverged rank)");
+  if (worst == RP_ABORT_PEER) return rp_fail(RP_ERR_ABORTED, "collective aborted by another rank");
+  return RP_OK;
+}
+
+static bool ready(rp_comm_t c) { return c && c->imported; }
+
+#define RP_REQUIRE_READY(c, name)                                                        \
+  do {                                                                                   \
+    if (!ready(c)) return rp_fail(RP_ERR_INVALID, std::string(name) + ": communicator not imported"); \
+    cudaSetDevice((c)->device);                                                          \
+  } while (0)
+
+int rp_all_reduce(rp_comm_t c, const void* src, void* dst, size_t count, int dtype_in, int dtype_comm,
+                  int dtype_out, int op, int algo, void* stream) {
+  RP_REQUIRE_READY(c, "rp_all_reduce");
+  if (c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_all_reduce: virtual communicator needs rp_all_reduce_v");
+  const void* s[1] = {src};
+  void* d[1] = {dst};
+  return rp_launch_all_reduce(c, s, d, count, dtype_in, dtype_comm, dtype_out, op, algo, (cudaStream_t)stream);
+}
+
+int rp_all_reduce_v(rp_comm_t c, const void* const* src, void* const* dst, size_t count, int dtype_in,
+                    int dtype_comm, int dtype_out, int op, int algo, void* stream) {
+  RP_REQUIRE_READY(c, "rp_all_reduce_v");
+  if (!c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_all_reduce_v: needs a virtual communicator");
+  return rp_launch_all_reduce(c, src, dst, count, dtype_in, dtype_comm, dtype_out, op, algo, (cudaStream_t)stream);
+}
+
+int rp_all_gather(rp_comm_t c, const void* src, void* dst, size_t bytes, void* stream) {
+  RP_REQUIRE_READY(c, "rp_all_gather");
+  if (c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_all_gather: virtual communicator needs rp_all_gather_v");
+  const void* s[1] = {src};
+  void* d[1] = {dst};
+  if (c->world == 1) {
+    if (dst != src) RP_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return RP_OK;
+  }
+  return rp_launch_all_gather(c, s, d, bytes, (cudaStream_t)stream);
+}
+
+int rp_all_gather_v(rp_comm_t c, const void* const* src, void* const* dst, size_t bytes, void* stream) {
+  RP_REQUIRE_READY(c, "rp_all_gather_v");
+  if (!c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_all_gather_v: needs a virtual communicator");
+  if (c->world == 1) {
+    if (dst[0] != src[0])
+      RP_CUDA_CHECK(cudaMemcpyAsync(dst[0], src[0], bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return RP_OK;
+  }
+  return rp_launch_all_gather(c, src, dst, bytes, (cudaStream_t)stream);
+}
+
+int rp_broadcast(rp_comm_t c, const void* src, void* dst, size_t bytes, int root, int algo, void* stream) {
+  RP_REQUIRE_READY(c, "rp_broadcast");
+  if (c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_broadcast: virtual communicator needs rp_broadcast_v");
+  if (c->world == 1) {
+    if (dst != src && src) RP_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return RP_OK;
+  }
+  const void* s[1] = {src ? src : dst};
+  void* d[1] = {dst};
+  return rp_launch_broadcast(c, s, d, bytes, root, algo, (cudaStream_t)stream);
+}
+
+int rp_broadcast_v(rp_comm_t c, const void* const* src, void* const* dst, size_t bytes, int root, int algo,
+                   void* stream) {
+  RP_REQUIRE_READY(c, "rp_broadcast_v");
+  if (!c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_broadcast_v: needs a virtual communicator");
+  if (c->world == 1) {
+    if (dst[0] != src[0])
+      RP_CUDA_CHECK(cudaMemcpyAsync(dst[0], src[0], bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return RP_OK;
+  }
+  return rp_launch_broadcast(c, src, dst, bytes, root, algo, (cudaStream_t)stream);
+}
+
+int rp_bn_stats(rp_comm_t c, const void* x, int dtype, int64_t rows, int64_t ch, int64_t hw, int layout,
+                float eps, float* mean, float* var, float* invstd, double* count, void* stream) {
+  RP_REQUIRE_READY(c, "rp_bn_stats");
+  return rp_launch_bn_stats(c, x, dtype, rows, ch, hw, layout, eps, mean, var, invstd, count, (cudaStream_t)stream);
+}
+
+int rp_bn_bwd_stats(rp_comm_t c, const void* x, const void* dy, int dtype, int64_t rows, int64_t ch, int64_t hw,
+                    int layout, const float* mean, float* sum_dy, float* sum_dy_xmu, float* local_sum_dy,
+                    float* local_sum_dy_xmu, void* stream) {
+  RP_REQUIRE_READY(c, "rp_bn_bwd_stats");
+  return rp_launch_bn_bwd_stats(c, x, dy, dtype, rows, ch, hw, layout, mean, sum_dy, sum_dy_xmu, local_sum_dy,
+                                local_sum_dy_xmu, (cudaStream_t)stream);
+}
+
+int rp_pack(void* dst, int dtype_dst, const void* const* ptrs, const int64_t* counts, const int64_t* offs, int n,
+            int dtype_src, void* stream) {
+  return pack_common(true, dst, dtype_dst, ptrs, counts, offs, n, dtype_src, (cudaStream_t)stream);
+}
+
+int rp_unpack(const void* src, int dtype_src, void* const* ptrs, const int64_t* counts, const int64_t* offs, int n,
+              int dtype_dst, void* stream) {
+  return pack_common(false, (void*)src, dtype_src, (const void* const*)ptrs, counts, offs, n, dtype_dst,
+                     (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+// Device-side building blocks: cross-GPU signalling, 128-bit vector access,
+// element conversions and the rank-ordered fold.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rp_internal.h"
+
+namespace rp {
+
+// ---------------------------------------------------------------------------
+// memory-model primitives (system scope: peers are other GPUs over NVLink)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 128-bit loads/stores. Peer data is read with plain weak loads after an
+// acquire (never .nc: peers write these buffers during the kernel).
+__device__ __forceinline__ uint4 ld128(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld128_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st128(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// cross-rank barrier: block b of every rank meets block b of every other rank
+// ---------------------------------------------------------------------------
+
+// Slot layout in each rank's signal region: sig[row * RP_MAX_RANKS + src_rank].
+// Thread p < world stores `value` into peer p's slot (row, rank) with release
+// semantics, then spins (acquire) until its own slot (row, p) reaches `value`.
+// Values are monotone per slot, so "reached" is a wrap-safe >= test.
+// Returns false if the wait timed out or a peer aborted (the block must bail).
+__device__ __forceinline__ bool rank_barrier(const RankTable& t, int world, uint64_t timeout_ns, int rank,
+                                             int row, uint32_t value) {
+  __shared__ int s_ok;
+  __syncthreads();  // all of this block's prior writes happen-before the release below
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < (unsigned)world) {
+    const int p = threadIdx.x;
+    st_release_sys(t.sig[p] + (size_t)row * RP_MAX_RANKS + rank, value);
+    const uint32_t* mine = t.sig[rank] + (size_t)row * RP_MAX_RANKS + p;
+    uint32_t* abort_word = t.sig[rank] + RP_ABORT_WORD;
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while ((int32_t)(ld_acquire_sys(mine) - value) < 0) {
+      if ((++spins & 255u) == 0) {
+        if (ld_relaxed_sys(abort_word) != 0) {  // a peer gave up: leave quickly
+          s_ok = 0;
+          break;
+        }
+        uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > timeout_ns) {
+          // record the timeout locally and tell every peer to stop waiting
+          atomicCAS(abort_word, 0u, RP_ABORT_TIMEOUT);
+          for (int q = 0; q < world; ++q)
+            if (q != rank) atomicCAS(t.sig[q] + RP_ABORT_WORD, 0u, RP_ABORT_PEER);
+          s_ok = 0;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+__device__ __forceinline__ bool rank_barrier(const CollArgs& a, int rank, int row, uint32_t value) {
+  return rank_barrier(a.t, a.world, a.timeout_ns, rank, row, value);
+}
+
+// ---------------------------------------------------------------------------
+// element types
+// ---------------------------------------------------------------------------
+
+template <int DT> struct DType;
+template <> struct DType<RP_F32> { using T = float;          using Acc = float;  static constexpr int kVec = 4; };
+template <> struct DType<RP_F64> { using T = double;         using Acc = double; static constexpr int kVec = 2; };
+template <> struct DType<RP_BF16> { using T = __nv_bfloat16; using Acc = float;  static constexpr int kVec = 8; };
+template <> struct DType<RP_F16> { using T = __half;         using Acc = float;  static constexpr int kVec = 8; };
+
+__device__ __forceinline__ float to_acc(float x) { return x; }
+__device__ __forceinline__ double to_acc(double x) { return x; }
+__device__ __forceinline__ float to_acc(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ float to_acc(__half x) { return __half2float(x); }
+
+template <typename T> __device__ __forceinline__ T from_f32(float x);
+template <> __device__ __forceinline__ float from_f32<float>(float x) { return x; }
+template <> __device__ __forceinline__ double from_f32<double>(float x) { return (double)x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ __half from_f32<__half>(float x) { return __float2half_rn(x); }
+
+template <typename T> __device__ __forceinline__ T from_acc(float x) { return from_f32<T>(x); }
+template <typename T> __device__ __forceinline__ T from_acc(double x) { return (T)x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(double x) { return __double2bfloat16(x); }
+template <> __device__ __forceinline__ __half from_acc<__half>(double x) { return __double2half(x); }
+
+// generic scalar conversion between any two element types (exact widening,
+// round-to-nearest-even narrowing)
+template <typename D, typename S> __device__ __forceinline__ D convert(S x) { return from_acc<D>(to_acc(x)); }
+template <> __device__ __forceinline__ float convert<float, double>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ double convert<double, float>(float x) { return (double)x; }
+
+// IEEE ops with contraction disabled (bit-exact with numpy's elementwise ops)
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+// np.maximum(a, b): a if (a > b or a is NaN) else b
+template <typename A> __device__ __forceinline__ A np_max(A a, A b) { return (a > b || a != a) ? a : b; }
+
+// Rank-ordered fold of OP, one element. `x` holds the N operands in rank order.
+template <int OP, typename A>
+struct Fold {
+  A acc;
+  A n;  // operand count as A (mean / premean divisor)
+  __device__ __forceinline__ void first(A x) { acc = (OP == RP_PREMEAN) ? div_rn(x, n) : x; }
+  __device__ __forceinline__ void next(A x) {
+    if (OP == RP_MAX) acc = np_max(acc, x);
+    else if (OP == RP_PREMEAN) acc = add_rn(acc, div_rn(x, n));
+    else acc = add_rn(acc, x);
+  }
+  __device__ __forceinline__ A result() const { return (OP == RP_MEAN) ? div_rn(acc, n) : acc; }
+};
+
+// Vector view of a 16-byte packet.
+template <typename T>
+union Pack16 {
+  uint4 u;
+  T e[16 / sizeof(T)];
+};
+
+}  // namespace rp

@@ -1,0 +1,124 @@
+// Internal definitions shared by the rp_* translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/rp.h"
+
+#define RP_MAX_RANKS 8
+// Signal slots: one row of RP_MAX_RANKS u32 per block index. Rows
+// [0, RP_MAX_BLOCKS) carry the per-block barriers of the collectives; rows
+// [RP_BN_ROW0, RP_BN_ROW0 + RP_BN_ROWS) those of the BN statistics exchange.
+#define RP_MAX_BLOCKS 1024
+#define RP_BN_ROW0 (RP_MAX_BLOCKS)
+#define RP_BN_ROWS 256
+#define RP_ABORT_WORD ((RP_MAX_BLOCKS + RP_BN_ROWS + 8) * RP_MAX_RANKS)  // u32 index
+#define RP_SIGNAL_BYTES (64 * 1024)  // signal region ahead of the data
+#define RP_ALIGN 256
+// The last RP_BN_BYTES of every pool hold the BN per-channel exchange records
+// (sum, sumsq, count as f64): up to RP_BN_ROWS*256 channels.
+#define RP_BN_BYTES ((size_t)RP_BN_ROWS * 256 * 3 * 8)
+#define RP_MIN_POOL ((size_t)4 << 20)
+
+// Abort reasons written into the abort word (first writer wins).
+#define RP_ABORT_TIMEOUT 1u
+#define RP_ABORT_PEER 2u
+
+struct RankTable {
+  char* data[RP_MAX_RANKS];       // data region base of every rank (peer-mapped)
+  uint32_t* sig[RP_MAX_RANKS];    // signal region base of every rank (peer-mapped)
+};
+
+struct rp_comm {
+  int rank = 0;
+  int world = 1;
+  int device = 0;
+  bool is_virtual = false;
+  bool imported = false;
+  size_t pool_bytes = 0;   // data bytes per rank
+  size_t reserved = 0;     // [0, reserved) belongs to the caller (fusion buckets)
+  char* alloc[RP_MAX_RANKS] = {};   // allocations owned by this process
+  bool ipc_opened[RP_MAX_RANKS] = {};
+  RankTable table{};
+  uint32_t epoch = 0;      // monotone barrier epoch (one increment per barrier use)
+  uint64_t timeout_ns = 20ull * 1000ull * 1000ull * 1000ull;
+  int num_sms = 148;
+  int max_coresident = 0;
+  // BN scratch: per-split f64 partials (device memory, all local replicas)
+  double* bn_partials = nullptr;
+  size_t bn_partials_bytes = 0;
+  // end of the staging window: the BN exchange records sit above it
+  size_t scratch_end() const { return pool_bytes - RP_BN_BYTES; }
+};
+
+// Export blob exchanged between ranks.
+struct RpExport {
+  uint64_t magic;
+  int32_t rank, world;
+  uint64_t pool_bytes;
+  cudaIpcMemHandle_t handle;
+  unsigned char uuid[16];
+  int32_t pci_bus, pci_device, pci_domain;
+};
+
+// Kernel argument block for the collectives (by value, < 4 KB).
+struct CollArgs {
+  RankTable t;
+  const void* src[RP_MAX_RANKS];
+  void* dst[RP_MAX_RANKS];
+  size_t read_off;      // pool offset holding (or receiving) each rank's input
+  size_t write_off;     // pool offset receiving the pushed result (two-shot)
+  size_t count;         // elements (all_reduce) or bytes (copy collectives)
+  size_t chunk;         // per-rank chunk (vectors or bytes) for partitioned phases
+  int world;
+  int rank;             // -1: virtual communicator, rank = blockIdx.y
+  int copy_in;          // stage src -> pool[read_off] inside the kernel
+  int copy_out;         // pool[write_off] -> dst inside the kernel
+  int dtype_in, dtype_out;
+  int root;
+  uint32_t epoch;       // barrier values epoch+1, epoch+2, ...
+  uint64_t timeout_ns;
+};
+
+// error plumbing
+void rp_set_error(const std::string& msg);
+int rp_fail(int code, const std::string& msg);
+#define RP_CUDA_CHECK(expr)                                                        \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return rp_fail(RP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+size_t rp_dtype_size(int dtype);
+// Make the device owning `p` current (entry points without a communicator).
+int rp_set_device_from_ptr(const void* p);
+bool rp_dtype_valid(int dtype);
+
+// launchers (defined in the .cu files)
+int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, size_t count,
+                         int dtype_in, int dtype_comm, int dtype_out, int op, int algo,
+                         cudaStream_t stream);
+int rp_launch_all_gather(rp_comm* c, const void* const* src, void* const* dst, size_t bytes,
+                         cudaStream_t stream);
+int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, size_t bytes,
+                        int root, int algo, cudaStream_t stream);
+int rp_launch_bn_stats(rp_comm* c, const void* x, int dtype, int64_t rows, int64_t ch, int64_t hw,
+                       int layout, float eps, float* mean, float* var, float* invstd, double* count,
+                       cudaStream_t stream);
+int rp_launch_bn_bwd_stats(rp_comm* c, const void* x, const void* dy, int dtype, int64_t rows,
+                           int64_t ch, int64_t hw, int layout, const float* mean, float* sum_dy,
+                           float* sum_dy_xmu, float* local_sum_dy, float* local_sum_dy_xmu,
+                           cudaStream_t stream);
+
+// Launch helper: cooperative launch for virtual communicators (all replicas'
+// blocks must be co-resident because they wait on one another), plain launch
+// otherwise (one rank per process; blocks only wait on peers' blocks).
+int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, size_t smem,
+              cudaStream_t stream);
+// Blocks per rank for a collective kernel given its per-block occupancy.
+int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want);
