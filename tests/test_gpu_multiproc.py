@@ -1,0 +1,241 @@
+"""Multi-process NVLink path: one process per GPU, communicators bootstrapped over
+torch.distributed (gloo, handle exchange only), kernels loading/storing peer pools.
+Needs >= 2 GPUs (``gpurun --gpus 2`` / ``--gpus 4``); skipped otherwise.
+
+Every rank derives all ranks' inputs from per-rank seeds, so each rank checks its
+own result against the CPU oracle on identical inputs (bit-exact folds / copies,
+1e-6 BN statistics)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+if NGPU < 2:
+    pytest.skip("needs >= 2 CUDA devices", allow_module_level=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, fn_name, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        globals()[fn_name](rank, world)
+        q.put((rank, None))
+    except BaseException as e:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(fn_name, world=None, timeout=600):
+    import torch.multiprocessing as mp
+
+    world = world or min(NGPU, 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn_name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    errs = {}
+    for _ in range(world):
+        r, err = q.get(timeout=timeout)
+        errs[r] = err
+    for p in procs:
+        p.join(timeout=60)
+    bad = {r: e for r, e in errs.items() if e}
+    assert not bad, "\n".join(f"rank {r}:\n{e}" for r, e in bad.items())
+
+
+# ---------------------------------------------------------------------------
+# rank bodies (module-level so spawn can pickle them by name)
+# ---------------------------------------------------------------------------
+
+def _inputs(world, count, dtype=np.float32, seed=100):
+    return [np.random.default_rng(seed + r).standard_normal(count).astype(dtype) for r in range(world)]
+
+
+def body_all_reduce(rank, world):
+    from oracle import collectives as O
+    from paper_1902_00465_b200.comm import Communicator
+
+    dev = torch.device(f"cuda:{rank}")
+    comm = Communicator(device=rank, pool_bytes=96 << 20)
+    for count in (1, 7, 1000, 4097, 1 << 16, (1 << 20) + 3, 16 << 20):
+        xs = _inputs(world, count, seed=count)
+        x = torch.from_numpy(xs[rank]).to(dev)
+        for kind in ("sum", "mean", "max", "premean"):
+            want = O.FOLDS[kind](xs)
+            for algo in ("oneshot", "twoshot"):
+                y = comm.all_reduce_tensor(x, kind, algo=algo)
+                got = y.cpu().numpy()
+                assert got.tobytes() == want.tobytes(), (count, kind, algo)
+    # f64 and bf16 with the fused exchange cast
+    xs = _inputs(world, 33333, np.float64, seed=7)
+    y = comm.all_reduce_tensor(torch.from_numpy(xs[rank]).to(dev), "sum")
+    assert y.cpu().numpy().tobytes() == O.fold_sum(xs).tobytes()
+    xs = _inputs(world, 50001, seed=8)
+    y = comm.all_reduce_tensor(torch.from_numpy(xs[rank]).to(dev), "premean", comm_dtype=torch.bfloat16)
+    want = O.bf16_bits_to_f32(O.fold_bf16([O.f32_to_bf16_bits(x) for x in xs], "premean"))
+    assert y.cpu().numpy().tobytes() == want.tobytes()
+    # zero-copy in place in the registered pool
+    buf = comm.alloc(1 << 20, torch.float32)
+    xs = _inputs(world, 1 << 20, seed=9)
+    buf.copy_(torch.from_numpy(xs[rank]))
+    comm.all_reduce_tensor(buf, "premean", out=buf)
+    assert buf.cpu().numpy().tobytes() == O.fold_premean(xs).tobytes()
+    comm.check()
+    comm.close()
+
+
+def body_gather_broadcast(rank, world):
+    from oracle import collectives as O
+    from paper_1902_00465_b200.comm import Communicator
+
+    dev = torch.device(f"cuda:{rank}")
+    comm = Communicator(device=rank, pool_bytes=64 << 20)
+    for count in (1, 7, 1000, 12345, 1 << 20):
+        xs = _inputs(world, count, seed=count + 1)
+        g = comm.all_gather_tensor(torch.from_numpy(xs[rank]).to(dev))
+        assert g.cpu().numpy().tobytes() == np.concatenate(xs).tobytes()
+        for root in range(world):
+            for algo in ("direct", "scatter"):
+                x = torch.from_numpy(xs[rank]).to(dev)
+                comm.broadcast_tensor(x, root=root, algo=algo)
+                assert x.cpu().numpy().tobytes() == xs[root].tobytes(), (count, root, algo)
+    # reference duck type with host values (graph.py:573-582)
+    xs = _inputs(world, 6, seed=3)
+    local = xs[rank].reshape(2, 3)
+    assert comm.all_reduce(local, "sum", "l").tobytes() == O.fold_sum([x.reshape(2, 3) for x in xs]).tobytes()
+    parts = comm.all_gather(local, "g")
+    assert all(p.tobytes() == xs[r].reshape(2, 3).tobytes() for r, p in enumerate(parts))
+    b = comm.broadcast(local if rank == 0 else None, "b", shape=(2, 3), dtype="f32")
+    assert b.tobytes() == xs[0].reshape(2, 3).tobytes()
+    comm.check()
+    comm.close()
+
+
+def body_bn(rank, world):
+    from oracle import collectives as O
+    from paper_1902_00465_b200.replicator import CrossReplicaBatchNorm, Replicator
+
+    dev = torch.device(f"cuda:{rank}")
+    repl = Replicator(device=rank, pool_bytes=16 << 20)
+    shape = (4, 16, 5, 5)
+    xs = [np.random.default_rng(50 + r).standard_normal(shape) * 2 + 1 for r in range(world)]
+    dys = [np.random.default_rng(60 + r).standard_normal(shape) for r in range(world)]
+    w = np.random.default_rng(70).standard_normal(16)
+    for fmt in (torch.contiguous_format, torch.channels_last):
+        bn = CrossReplicaBatchNorm(16, repl).to(dev)
+        with torch.no_grad():
+            bn.weight.copy_(torch.from_numpy(w))
+        x = torch.from_numpy(xs[rank]).float().to(dev).contiguous(memory_format=fmt).requires_grad_(True)
+        y = bn(x)
+        y.backward(torch.from_numpy(dys[rank]).float().to(dev).contiguous(memory_format=fmt))
+        outs, mean, var, _ = O.bn_forward_per_channel(xs, "nchw", weight=w, bias=np.zeros(16))
+        np.testing.assert_allclose(y.detach().cpu().numpy(), outs[rank], rtol=1e-4, atol=1e-4)
+        dxs, sdy, sdyx = O.bn_backward_per_channel(xs, dys, "nchw", weight=w)
+        np.testing.assert_allclose(x.grad.cpu().numpy(), dxs[rank], rtol=1e-4, atol=1e-4)
+        # local weight/bias grads (averaged later by the wrapped optimizer)
+        xr = O._channel_view(xs[rank], "nchw")
+        dr = O._channel_view(dys[rank], "nchw")
+        np.testing.assert_allclose(bn.bias.grad.cpu().numpy(), dr.sum(0), rtol=1e-5, atol=1e-4)
+        np.testing.assert_allclose(bn.weight.grad.cpu().numpy(), (dr * (xr - mean) / np.sqrt(var + 1e-5)).sum(0),
+                                   rtol=1e-4, atol=1e-4)
+        np.testing.assert_allclose(bn.running_mean.cpu().numpy(), 0.1 * mean, rtol=1e-5, atol=1e-6)
+    repl.comm.close()
+
+
+def body_wrap_optimizer(rank, world):
+    from paper_1902_00465_b200.replicator import Replicator
+
+    dev = torch.device(f"cuda:{rank}")
+    repl = Replicator(device=rank, pool_bytes=32 << 20)
+    torch.manual_seed(rank)  # deliberately different init: replicate() must broadcast replica 0
+    with repl.context():
+        model = repl.replicate(lambda: torch.nn.Sequential(torch.nn.Linear(784, 256), torch.nn.ReLU(),
+                                                           torch.nn.Linear(256, 10)).double())
+        opt = repl.wrap_optimizer(torch.optim.SGD(model.parameters(), lr=0.1))
+    # single-device oracle: the same model trained on the concatenated batch
+    torch.manual_seed(0)
+    ref = torch.nn.Sequential(torch.nn.Linear(784, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).double().to(dev)
+    with torch.no_grad():
+        for p, q in zip(ref.parameters(), model.local.parameters()):
+            p.copy_(q)
+    ref_opt = torch.optim.SGD(ref.parameters(), lr=0.1)
+    B = 16
+    for step in range(5):
+        g = torch.Generator().manual_seed(step)
+        xs = torch.randn(world * B, 784, generator=g, dtype=torch.float64).to(dev)
+        ys = torch.randint(0, 10, (world * B,), generator=g).to(dev)
+        opt.zero_grad()
+        loss = torch.nn.functional.cross_entropy(model(xs[rank * B:(rank + 1) * B]), ys[rank * B:(rank + 1) * B])
+        loss.backward()
+        opt.step()
+        ref_opt.zero_grad()
+        torch.nn.functional.cross_entropy(ref(xs), ys).backward()
+        ref_opt.step()
+    for p, q in zip(model.local.parameters(), ref.parameters()):
+        assert (p - q).abs().max().item() < 1e-9  # SPEC.md:399 sync-equivalence bound
+    # replicas bit-identical
+    flat = torch.cat([p.detach().reshape(-1) for p in model.local.parameters()])
+    g = repl.comm.all_gather_tensor(flat)
+    for r in range(world):
+        assert torch.equal(g[r], g[0])
+    repl.comm.close()
+
+
+def body_timeout(rank, world):
+    """A rank that never joins makes the others time out (not hang) and report
+    CollectiveAbortedError (SPEC.md:237 liveness; errors.py:68)."""
+    from paper_1902_00465_b200 import errors
+    from paper_1902_00465_b200.comm import Communicator
+
+    comm = Communicator(device=rank, pool_bytes=8 << 20, timeout_s=2.0)
+    x = torch.ones(1024, device=f"cuda:{rank}")
+    if rank != world - 1:
+        comm.all_reduce_tensor(x, "sum")
+        with pytest.raises(errors.CollectiveAbortedError):
+            comm.check()
+    import torch.distributed as dist
+    dist.barrier()
+    comm.close()
+
+
+# ---------------------------------------------------------------------------
+
+def test_all_reduce_multiprocess():
+    run_world("body_all_reduce")
+
+
+def test_gather_broadcast_multiprocess():
+    run_world("body_gather_broadcast")
+
+
+def test_cross_replica_bn_autograd_multiprocess():
+    run_world("body_bn")
+
+
+def test_wrap_optimizer_sync_equivalence_multiprocess():
+    run_world("body_wrap_optimizer")
+
+
+def test_dead_rank_times_out():
+    run_world("body_timeout")
