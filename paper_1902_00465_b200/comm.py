@@ -75,6 +75,19 @@ def tensor_at(ptr: int, numel: int, dtype: torch.dtype, device: int, owner) -> t
     return raw.view(dtype)
 
 
+def exchange_blobs(blob: bytes, group=None) -> bytes:
+    """Bootstrap exchange: every rank's export blob, concatenated in rank order.
+    The only use of torch.distributed (any backend); never on a data path."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, bytes(blob), group=group)
+    if any(len(b) != len(blob) for b in blobs):
+        raise errors.ProtocolError("ranks exported blobs of different sizes (mismatched library builds?)")
+    return b"".join(blobs)
+
+
 class _Base:
     """State shared by the multi-process and the virtual communicator."""
 
@@ -168,9 +181,7 @@ class Communicator(_Base):
             buf = ctypes.create_string_buffer(size)
             n = ctypes.c_size_t(size)
             _lib.check(lib.rp_comm_export(h, buf, ctypes.byref(n)), "comm_export")
-            blobs = [None] * world
-            dist.all_gather_object(blobs, bytes(buf.raw[: n.value]), group=group)
-            joined = b"".join(blobs)
+            joined = exchange_blobs(bytes(buf.raw[: n.value]), group)
             _lib.check(lib.rp_comm_import(h, joined, len(joined)), "comm_import")
         self._init_common(pool_bytes, timeout_s)
 

@@ -82,11 +82,26 @@ class _Rendezvous:
         self.slots: dict[int, tuple] = {}
         self.results = None
         self.error = None
+        self.broken: BaseException | None = None  # a replica died: fail every later arrival
         self.gen = 0
         self.seq = 0
 
+    def reset(self):
+        with self.cv:
+            self.slots, self.results, self.error, self.broken = {}, None, None, None
+
+    def abort(self, e: BaseException):
+        with self.cv:
+            self.broken = e
+            self.slots = {}
+            self.gen += 1
+            self.cv.notify_all()
+
     def __call__(self, r, desc, value, fn):
         with self.cv:
+            if self.broken is not None:
+                raise errors.CollectiveAbortedError(
+                    f"replica {r}: collective {desc} aborted, another replica failed: {self.broken!r}")
             gen = self.gen
             if r in self.slots:
                 raise errors.ProtocolError(f"replica {r} entered collective {desc} twice")
@@ -110,6 +125,9 @@ class _Rendezvous:
             else:
                 if not self.cv.wait_for(lambda: self.gen != gen, timeout=600):
                     raise errors.CollectiveAbortedError(f"replica {r} timed out in collective {desc}")
+                if self.broken is not None:
+                    raise errors.CollectiveAbortedError(
+                        f"replica {r}: collective {desc} aborted, another replica failed: {self.broken!r}")
             if self.error is not None:
                 raise self.error
             return self.results[r]
@@ -260,6 +278,7 @@ class Replicator:
             return [one(self.comm.rank)]
         n = self.comm.world
         results, errs = [None] * n, [None] * n
+        self._rv.reset()
 
         def worker(r):
             _tls.replica = r
@@ -268,20 +287,16 @@ class Replicator:
                     results[r] = one(r)
             except BaseException as e:
                 errs[r] = e
-                with self._rv.cv:  # unblock the others
-                    self._rv.error = e
-                    self._rv.gen += 1
-                    self._rv.slots = {}
-                    self._rv.cv.notify_all()
+                self._rv.abort(e)  # unblock waiting replicas and fail late arrivals
 
         threads = [threading.Thread(target=worker, args=(r,), name=f"replica-{r}") for r in range(n)]
         for t in threads:
             t.start()
         for t in threads:
             t.join()
-        for e in errs:
-            if e is not None:
-                raise e
+        root = [e for e in errs if e is not None and not isinstance(e, errors.CollectiveAbortedError)]
+        if root or any(e is not None for e in errs):
+            raise (root or [e for e in errs if e is not None])[0]
         return results
 
     # -- primitives --------------------------------------

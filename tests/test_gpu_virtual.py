@@ -344,8 +344,9 @@ def test_bn_apply_kernels_match_torch():
 # --- the Replicator facade on virtual replicas ----------------------------------
 
 def test_wrap_optimizer_matches_reference_bitwise(wrap_golden):
+    wrap_golden = {k: wrap_golden[k] for k in wrap_golden.files}  # NpzFile is not thread-safe
     for n in (2, 4):
-        nw = len([k for k in wrap_golden.files if k.startswith(f"small_n{n}_w")])
+        nw = len([k for k in wrap_golden if k.startswith(f"small_n{n}_w")])
         repl = Replicator(num_replicas=n, device=0, pool_bytes=8 << 20)
         with repl.context():
             params = repl.replicate(lambda: torch.nn.ParameterList(

@@ -1,0 +1,189 @@
+"""Host-side logic and the C-ABI boundary, on CPU: the library loads and exports every
+symbol include/rp.h declares (no compute calls), status codes map onto the reference's
+exception classes, the virtual-replica rendezvous enforces the stitcher's agreement
+check, and the multi-process bootstrap exchange works at world_size 2 over gloo."""
+
+import os
+import re
+import socket
+import threading
+
+import pytest
+import torch
+
+from paper_1902_00465_b200 import _lib, errors
+from tests.helpers import ROOT
+
+HEADER = os.path.join(ROOT, "include", "rp.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"RP_API\s+[\w\s\*]+?\b(rp_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = header_functions()
+    for required in ("rp_comm_create", "rp_comm_import", "rp_all_reduce", "rp_all_gather", "rp_broadcast",
+                     "rp_bn_stats", "rp_bn_bwd_stats", "rp_pack", "rp_unpack", "rp_last_error"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    names = header_functions()
+    assert sorted(_lib.SIGNATURES) == names, "ctypes table must mirror include/rp.h"
+    for n in names:
+        assert hasattr(lib, n), n
+    assert lib.rp_version().decode().endswith("sm_100a")
+    assert lib.rp_comm_export_size() > 64
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    monkeypatch.setattr(_lib, "_LIB", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/librp.so")
+    with pytest.raises(errors.NativeLibraryError):
+        _lib.load()
+
+
+def test_status_codes_map_to_reference_exceptions():
+    _lib.load()
+    for code, cls in [(1, errors.ShapeError), (2, errors.ConfigurationError), (3, errors.CollectiveError),
+                      (4, errors.CollectiveAbortedError), (5, errors.ProtocolError)]:
+        with pytest.raises(cls):
+            _lib.check(code, "x")
+    _lib.check(0)
+    # hierarchy as in the reference's errors.py:4-81
+    assert issubclass(errors.ProtocolError, errors.CollectiveError)
+    assert issubclass(errors.CollectiveAbortedError, errors.CollectiveError)
+    assert issubclass(errors.CollectiveError, errors.ReplicatorError)
+    assert issubclass(errors.ShapeError, errors.GraphError)
+
+
+def test_c_abi_rejects_bad_arguments_without_a_gpu():
+    """Argument validation runs before any CUDA call."""
+    import ctypes
+    lib = _lib.load()
+    assert lib.rp_comm_create(0, 9, 0, 64 << 20, ctypes.byref(ctypes.c_void_p())) == 2   # world > 8
+    assert lib.rp_comm_create(0, 2, 0, 1 << 20, ctypes.byref(ctypes.c_void_p())) == 1    # pool < 4 MiB
+    assert "pool_bytes" in _lib.last_error()
+    assert lib.rp_comm_create_virtual(0, 0, 64 << 20, ctypes.byref(ctypes.c_void_p())) == 2
+    assert lib.rp_all_reduce(None, None, None, 1, 0, 0, 0, 0, 0, None) == 1            # NULL comm
+
+
+# --- virtual-replica rendezvous ------------------------------------------------
+
+def _run_threads(n, body):
+    errs = [None] * n
+    out = [None] * n
+
+    def w(r):
+        try:
+            out[r] = body(r)
+        except BaseException as e:  # noqa: BLE001
+            errs[r] = e
+    ts = [threading.Thread(target=w, args=(r,)) for r in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=30)
+    return out, errs
+
+
+def test_rendezvous_runs_once_for_all_replicas():
+    from paper_1902_00465_b200.replicator import _Rendezvous
+    rv = _Rendezvous(4)
+    calls = []
+
+    def fused(values):
+        calls.append(list(values))
+        return [sum(values)] * 4
+
+    out, errs = _run_threads(4, lambda r: rv(r, ("all_reduce", "g", (3,)), r + 1, fused))
+    assert errs == [None] * 4
+    assert out == [10] * 4 and calls == [[1, 2, 3, 4]]  # all_sum 1..4 -> 10
+
+
+def test_rendezvous_first_divergence_is_protocol_error():
+    from paper_1902_00465_b200.replicator import _Rendezvous
+    rv = _Rendezvous(2)
+    out, errs = _run_threads(2, lambda r: rv(r, ("all_reduce", "a" if r == 0 else "b"), r, lambda v: v))
+    assert all(isinstance(e, errors.ProtocolError) for e in errs)
+    assert "first divergence" in str(errs[0])
+
+
+def test_rendezvous_abort_fails_late_arrivals_fast():
+    from paper_1902_00465_b200.replicator import _Rendezvous
+    rv = _Rendezvous(3)
+    rv.abort(RuntimeError("replica 2 died"))
+    out, errs = _run_threads(2, lambda r: rv(r, ("x",), r, lambda v: v))
+    assert all(isinstance(e, errors.CollectiveAbortedError) for e in errs)
+
+
+def test_label_reuse_within_a_generation_is_rejected():
+    from paper_1902_00465_b200.comm import _Base
+    b = _Base()
+    b._labels, b.check_labels = set(), True
+    b._use_label("g0")
+    with pytest.raises(errors.ProtocolError):
+        b._use_label("g0")
+    b.new_generation()
+    b._use_label("g0")                # reuse across generations is fine
+
+
+def test_bn_layout_detection():
+    from paper_1902_00465_b200.replicator import _bn_layout
+    assert _bn_layout(torch.empty(8, 3)) == (_lib.NHWC, 8, 3, 1)
+    assert _bn_layout(torch.empty(2, 3, 4, 5)) == (_lib.NCHW, 2, 3, 20)
+    cl = torch.empty(2, 3, 4, 5).contiguous(memory_format=torch.channels_last)
+    assert _bn_layout(cl) == (_lib.NHWC, 40, 3, 1)
+    assert _bn_layout(torch.empty(2, 3, 4, 5).transpose(2, 3)) is None
+
+
+# --- world_size 2 over gloo: bootstrap exchange ----------------------------------
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1902_00465_b200.comm import exchange_blobs
+        joined = exchange_blobs(bytes([rank]) * 16)
+        ok = joined == b"".join(bytes([r]) * 16 for r in range(world))
+        try:
+            exchange_blobs(bytes([rank]) * (16 + rank))
+            bad = False
+        except errors.ProtocolError:
+            bad = True
+        q.put((rank, ok and bad))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bootstrap_exchange_world2_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=30)
+    assert res == {0: True, 1: True}
