@@ -112,8 +112,7 @@ __device__ __forceinline__ uint4 fold_packet(const uint4 (&x)[NR]) {
   Pack16<T> out;
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
-    Fold<OP, A> f;
-    f.n = (A)NR;
+    Fold<OP, A, NR> f;
     Pack16<T> p0;
     p0.u = x[0];
     f.first(to_acc(p0.e[e]));

@@ -147,18 +147,30 @@ __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(
 // np.maximum(a, b): a if (a > b or a is NaN) else b
 template <typename A> __device__ __forceinline__ A np_max(A a, A b) { return (a > b || a != a) ? a : b; }
 
-// Rank-ordered fold of OP, one element. `x` holds the N operands in rank order.
-template <int OP, typename A>
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// x / NR correctly rounded. For a power-of-two NR the exact quotient equals the
+// exact product x * (1/NR), so the (correctly rounded) multiply is bit-identical to
+// the division -- subnormals included -- at a fraction of the instructions.
+template <int NR, typename A>
+__device__ __forceinline__ A div_count(A x) {
+  if constexpr ((NR & (NR - 1)) == 0) return mul_rn(x, (A)1 / (A)NR);
+  else return div_rn(x, (A)NR);
+}
+
+// Rank-ordered fold of OP over NR operands, one element (graph.py:514-528,
+// SPEC.md:406): first() takes rank 0's operand, next() ranks 1..NR-1 in order.
+template <int OP, typename A, int NR>
 struct Fold {
   A acc;
-  A n;  // operand count as A (mean / premean divisor)
-  __device__ __forceinline__ void first(A x) { acc = (OP == RP_PREMEAN) ? div_rn(x, n) : x; }
+  __device__ __forceinline__ void first(A x) { acc = (OP == RP_PREMEAN) ? div_count<NR>(x) : x; }
   __device__ __forceinline__ void next(A x) {
     if (OP == RP_MAX) acc = np_max(acc, x);
-    else if (OP == RP_PREMEAN) acc = add_rn(acc, div_rn(x, n));
+    else if (OP == RP_PREMEAN) acc = add_rn(acc, div_count<NR>(x));
     else acc = add_rn(acc, x);
   }
-  __device__ __forceinline__ A result() const { return (OP == RP_MEAN) ? div_rn(acc, n) : acc; }
+  __device__ __forceinline__ A result() const { return (OP == RP_MEAN) ? div_count<NR>(acc) : acc; }
 };
 
 // Vector view of a 16-byte packet.
