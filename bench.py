@@ -214,6 +214,12 @@ def run_ours(args, rank, world, local):
         def step():
             comm.all_reduce_tensor(buf, args.kind, out=buf, algo=args.algo)
 
+    align = None
+    if world > 1:
+        tiny = torch.zeros(4, device=dev)
+
+        def align():
+            comm.all_reduce_tensor(tiny, "sum", out=tiny)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -234,6 +240,8 @@ def run_ours(args, rank, world, local):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.zero_()
+        if align is not None:
+            align()  # untimed tiny collective: ranks leave the flush together (no skew in the step)
         evs[i][0].record(stream)
         step()
         evs[i][1].record(stream)

@@ -1,4 +1,6 @@
 // Instantiates the all-reduce kernels for the bf16 exchange dtype.
 #include "rp_allreduce.cuh"
 
-const void* rp_pick_ar_bf16(int op, int algo, int world) { return rp::pick_ar_op<RP_BF16>(op, algo, world); }
+const void* rp_pick_ar_bf16(int op, int algo, int world, int push) {
+  return rp::pick_ar_op<RP_BF16>(op, algo, world, push);
+}

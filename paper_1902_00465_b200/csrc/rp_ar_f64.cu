@@ -1,4 +1,6 @@
 // Instantiates the all-reduce kernels for the f64 exchange dtype.
 #include "rp_allreduce.cuh"
 
-const void* rp_pick_ar_f64(int op, int algo, int world) { return rp::pick_ar_op<RP_F64>(op, algo, world); }
+const void* rp_pick_ar_f64(int op, int algo, int world, int push) {
+  return rp::pick_ar_op<RP_F64>(op, algo, world, push);
+}

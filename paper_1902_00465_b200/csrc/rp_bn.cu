@@ -445,7 +445,7 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   ExArgs e;
   memset(&e, 0, sizeof(e));
   e.t = c->table;
-  e.bn_off = c->scratch_end();
+  e.bn_off = c->bn_records();
   e.C = ch;
   e.S = a.S;
   e.world = W;

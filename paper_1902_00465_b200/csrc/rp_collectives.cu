@@ -14,24 +14,30 @@
 // rp_device.cuh). Replaces the reference's in-process folds (graph.py:506-540),
 // the mesh seam's communicator calls (graph.py:565-583) and the SPEC ring
 // (SPEC.md:188-222).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "rp_device.cuh"
 
-const void* rp_pick_ar_f32(int op, int algo, int world);
-const void* rp_pick_ar_f64(int op, int algo, int world);
-const void* rp_pick_ar_bf16(int op, int algo, int world);
-const void* rp_pick_ar_f16(int op, int algo, int world);
+const void* rp_pick_ar_f32(int op, int algo, int world, int push);
+const void* rp_pick_ar_f64(int op, int algo, int world, int push);
+const void* rp_pick_ar_bf16(int op, int algo, int world, int push);
+const void* rp_pick_ar_f16(int op, int algo, int world, int push);
 
-static const void* pick_ar_any(int dtype, int op, int algo, int world) {
+static const void* pick_ar_any(int dtype, int op, int algo, int world, int push) {
   switch (dtype) {
-    case RP_F32: return rp_pick_ar_f32(op, algo, world);
-    case RP_F64: return rp_pick_ar_f64(op, algo, world);
-    case RP_BF16: return rp_pick_ar_bf16(op, algo, world);
-    case RP_F16: return rp_pick_ar_f16(op, algo, world);
+    case RP_F32: return rp_pick_ar_f32(op, algo, world, push);
+    case RP_F64: return rp_pick_ar_f64(op, algo, world, push);
+    case RP_BF16: return rp_pick_ar_bf16(op, algo, world, push);
+    case RP_F16: return rp_pick_ar_f16(op, algo, world, push);
   }
   return nullptr;
 }
+
+struct CollArgs;
+static int launch_push(rp_comm* c, const void* const* src, void* const* dst, size_t count, int dtype_in,
+                       int dtype_comm, int dtype_out, int op, int algo, cudaStream_t stream, CollArgs a);
 
 namespace rp {
 
@@ -230,7 +236,7 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   a.copy_in = a.copy_out = 0;
 
   if (W == 1) {  // a single replica: the fold of one operand (identity / x/1)
-    const void* fn = pick_ar_any(dtype_comm, op, RP_ALGO_TWOSHOT, 1);
+    const void* fn = pick_ar_any(dtype_comm, op, RP_ALGO_TWOSHOT, 1, 0);
     a.src[0] = src[0];
     a.dst[0] = dst[0];
     const int blocks = (int)std::min<size_t>((V + kThreads - 1) / kThreads, (size_t)c->num_sms * 4);
@@ -247,6 +253,14 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   }
   if (algo != RP_ALGO_ONESHOT && algo != RP_ALGO_TWOSHOT)
     return rp_fail(RP_ERR_INVALID, "all_reduce: unknown algorithm");
+
+  // Data-movement form. Push (only stores cross NVLink, every fold reads local
+  // HBM; measured bidirectional peer STG 690 vs LDG 650 GB/s, tools/nvlink_probe)
+  // for one-process-per-GPU communicators; pull (each buffer read and written
+  // exactly once: the HBM-minimal form) for virtual replicas sharing one GPU.
+  int push = c->is_virtual ? 0 : 1;
+  if (const char* e = getenv("RP_AR_IMPL")) push = (e[0] == 'p' && e[1] == 'u' && e[2] == 's') ? 1 : 0;
+  if (push) return launch_push(c, src, dst, count, dtype_in, dtype_comm, dtype_out, op, algo, stream, a);
 
   // Placement. Pool-resident buffers (symmetric offsets, allocated identically on
   // every rank) are exchanged zero-copy; anything else is staged through scratch.
@@ -310,7 +324,7 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
     return RP_OK;
   }
 
-  const void* fn = pick_ar_any(dtype_comm, op, algo, W);
+  const void* fn = pick_ar_any(dtype_comm, op, algo, W, 0);
   if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
 
   size_t work;  // vectors one rank's blocks cover
@@ -324,7 +338,76 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   int blocks = (int)std::min<size_t>((work + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
   blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
   a.epoch = c->epoch;
-  c->epoch += 2;
+  c->epoch += (algo == RP_ALGO_TWOSHOT && a.copy_out) ? 3 : 2;
+  c->calls += 1;
+  void* args[] = {&a};
+  return rp_launch(c, fn, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads), args, 0, stream);
+}
+
+// Push-form all-reduce (K1p one-shot / K2p two-shot, rp_allreduce.cuh).
+static int launch_push(rp_comm* c, const void* const* src, void* const* dst, size_t count, int dtype_in,
+                       int dtype_comm, int dtype_out, int op, int algo, cudaStream_t stream, CollArgs a) {
+  const int W = c->world;
+  const int nrep = c->is_virtual ? W : 1;
+  const size_t vec = 16 / rp_dtype_size(dtype_comm);
+  const size_t V = (count + vec - 1) / vec;
+  // one-shot landing zone: W slots of V vectors must fit one parity region
+  if (algo == RP_ALGO_ONESHOT && (size_t)W * V * 16 > RP_OS_REGION) algo = RP_ALGO_TWOSHOT;
+  const size_t scratch = round_up(c->reserved, RP_ALIGN);
+  const size_t scratch_end = c->scratch_end();
+  int epochs;
+  size_t work;
+  if (algo == RP_ALGO_ONESHOT) {
+    a.read_off = c->oneshot_zone((int)(c->calls & 1));
+    a.copy_out = 1;
+    a.chunk = 0;
+    work = V;
+    epochs = 1;
+  } else {
+    const size_t Vc = (V + W - 1) / W;
+    const size_t qbytes = round_up((size_t)W * Vc * 16, RP_ALIGN);
+    size_t dst_off = 0;
+    const bool dst_pool = dtype_out == dtype_comm &&
+                          symmetric_in_pool(c, (const void* const*)dst, count * rp_dtype_size(dtype_out), &dst_off) &&
+                          dst_off + round_up(V * 16, RP_ALIGN) <= scratch;
+    const size_t need = qbytes + (dst_pool ? 0 : qbytes);
+    if (scratch + need > scratch_end) {
+      // pieces that fit the staging window (each piece is a full collective)
+      const size_t avail = scratch_end > scratch ? scratch_end - scratch : 0;
+      size_t piece = (avail / (dst_pool ? 1 : 2) / 16) * vec;
+      piece -= piece % ((size_t)W * vec * 64);
+      if (piece == 0) return rp_fail(RP_ERR_INVALID, "all_reduce: pool too small to stage the message");
+      for (size_t off = 0; off < count; off += piece) {
+        const size_t n = std::min(piece, count - off);
+        const void* s2[RP_MAX_RANKS];
+        void* d2[RP_MAX_RANKS];
+        for (int i = 0; i < nrep; ++i) {
+          s2[i] = (const char*)src[i] + off * rp_dtype_size(dtype_in);
+          d2[i] = (char*)dst[i] + off * rp_dtype_size(dtype_out);
+        }
+        CollArgs a2 = a;
+        fill_ptrs(c, a2, s2, d2);
+        const int rc = launch_push(c, s2, d2, n, dtype_in, dtype_comm, dtype_out, op, algo, stream, a2);
+        if (rc) return rc;
+      }
+      return RP_OK;
+    }
+    a.chunk = Vc;
+    a.read_off = scratch;
+    a.write_off = dst_pool ? dst_off : scratch + qbytes;
+    a.copy_out = dst_pool ? 0 : 1;
+    work = Vc;
+    epochs = dst_pool ? 2 : 3;
+  }
+  a.count = count;
+  const void* fn = pick_ar_any(dtype_comm, op, algo, W, 1);
+  if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
+  const size_t per_block = (size_t)kThreads * 2;
+  int blocks = (int)std::min<size_t>((work + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
+  blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
+  a.epoch = c->epoch;
+  c->epoch += epochs;
+  c->calls += 1;
   void* args[] = {&a};
   return rp_launch(c, fn, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads), args, 0, stream);
 }

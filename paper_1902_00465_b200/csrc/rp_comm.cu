@@ -224,7 +224,7 @@ int rp_comm_create(int rank, int world, int device, size_t pool_bytes, rp_comm_t
   if (!out) return rp_fail(RP_ERR_INVALID, "rp_comm_create: out is NULL");
   if (world < 1 || world > RP_MAX_RANKS || rank < 0 || rank >= world)
     return rp_fail(RP_ERR_CONFIG, "rp_comm_create: need 1 <= world <= 8 and 0 <= rank < world");
-  if (pool_bytes < RP_MIN_POOL) return rp_fail(RP_ERR_INVALID, "rp_comm_create: pool_bytes must be >= 4 MiB");
+  if (pool_bytes < RP_MIN_POOL) return rp_fail(RP_ERR_INVALID, "rp_comm_create: pool_bytes must be >= 16 MiB");
   rp_comm* c = new rp_comm();
   c->rank = rank;
   c->world = world;
@@ -244,7 +244,7 @@ int rp_comm_create(int rank, int world, int device, size_t pool_bytes, rp_comm_t
 int rp_comm_create_virtual(int world, int device, size_t pool_bytes, rp_comm_t* out) {
   if (!out) return rp_fail(RP_ERR_INVALID, "rp_comm_create_virtual: out is NULL");
   if (world < 1 || world > RP_MAX_RANKS) return rp_fail(RP_ERR_CONFIG, "virtual world must be 1..8");
-  if (pool_bytes < RP_MIN_POOL) return rp_fail(RP_ERR_INVALID, "rp_comm_create_virtual: pool_bytes must be >= 4 MiB");
+  if (pool_bytes < RP_MIN_POOL) return rp_fail(RP_ERR_INVALID, "rp_comm_create_virtual: pool_bytes must be >= 16 MiB");
   rp_comm* c = new rp_comm();
   c->world = world;
   c->device = device;

@@ -19,10 +19,19 @@
 #define RP_ABORT_WORD ((RP_MAX_BLOCKS + RP_BN_ROWS + 8) * RP_MAX_RANKS)  // u32 index
 #define RP_SIGNAL_BYTES (64 * 1024)  // signal region ahead of the data
 #define RP_ALIGN 256
-// The last RP_BN_BYTES of every pool hold the BN per-channel exchange records
-// (sum, sumsq, count as f64): up to RP_BN_ROWS*256 channels.
+// Pool layout (every rank identical):
+//   [0, reserved)                          caller buffers (fusion buckets), zero-copy
+//   [reserved, scratch_end)                general staging (two-shot Q / W, pull staging)
+//   [scratch_end, +2*RP_OS_REGION)         one-shot push landing zones, parity 0 / 1
+//   [pool_bytes - RP_BN_BYTES, pool_bytes) BN per-channel exchange records
+// Kernels may read their pool after their LAST barrier only from the one-shot
+// landing zones (double-buffered by call parity); everything else is protected
+// by a trailing barrier, so a peer that already started the next call and
+// pushes without a start barrier can never clobber data still being read.
+// The BN records hold (sum, sumsq, count) as f64 for up to RP_BN_ROWS*256 channels.
 #define RP_BN_BYTES ((size_t)RP_BN_ROWS * 256 * 3 * 8)
-#define RP_MIN_POOL ((size_t)4 << 20)
+#define RP_OS_REGION ((size_t)4 << 20)
+#define RP_MIN_POOL ((size_t)16 << 20)
 
 // Abort reasons written into the abort word (first writer wins).
 #define RP_ABORT_TIMEOUT 1u
@@ -51,8 +60,11 @@ struct rp_comm {
   // BN scratch: per-split f64 partials (device memory, all local replicas)
   double* bn_partials = nullptr;
   size_t bn_partials_bytes = 0;
-  // end of the staging window: the BN exchange records sit above it
-  size_t scratch_end() const { return pool_bytes - RP_BN_BYTES; }
+  uint32_t calls = 0;      // collective calls issued (one-shot landing-zone parity)
+  // end of the general staging window (see the layout above)
+  size_t scratch_end() const { return pool_bytes - RP_BN_BYTES - 2 * RP_OS_REGION; }
+  size_t oneshot_zone(int parity) const { return scratch_end() + (size_t)parity * RP_OS_REGION; }
+  size_t bn_records() const { return pool_bytes - RP_BN_BYTES; }
 };
 
 // Export blob exchanged between ranks.

@@ -78,15 +78,21 @@ def body_all_reduce(rank, world):
 
     dev = torch.device(f"cuda:{rank}")
     comm = Communicator(device=rank, pool_bytes=96 << 20)
-    for count in (1, 7, 1000, 4097, 1 << 16, (1 << 20) + 3, 16 << 20):
-        xs = _inputs(world, count, seed=count)
-        x = torch.from_numpy(xs[rank]).to(dev)
-        for kind in ("sum", "mean", "max", "premean"):
-            want = O.FOLDS[kind](xs)
-            for algo in ("oneshot", "twoshot"):
-                y = comm.all_reduce_tensor(x, kind, algo=algo)
-                got = y.cpu().numpy()
-                assert got.tobytes() == want.tobytes(), (count, kind, algo)
+    for impl in ("push", "pull"):
+        os.environ["RP_AR_IMPL"] = impl
+        for count in (1, 7, 1000, 4097, 1 << 16, (1 << 20) + 3, 16 << 20, 40 << 20):
+            xs = _inputs(world, count, seed=count)
+            x = torch.from_numpy(xs[rank]).to(dev)
+            for kind in ("sum", "mean", "max", "premean"):
+                want = O.FOLDS[kind](xs)
+                for algo in ("oneshot", "twoshot"):
+                    y = comm.all_reduce_tensor(x, kind, algo=algo)
+                    got = y.cpu().numpy()
+                    assert got.tobytes() == want.tobytes(), (impl, count, kind, algo)
+                    y2 = x.clone()
+                    comm.all_reduce_tensor(y2, kind, out=y2, algo=algo)  # in place, user buffer
+                    assert y2.cpu().numpy().tobytes() == want.tobytes(), (impl, count, kind, algo, "inplace")
+    os.environ.pop("RP_AR_IMPL")
     # f64 and bf16 with the fused exchange cast
     xs = _inputs(world, 33333, np.float64, seed=7)
     y = comm.all_reduce_tensor(torch.from_numpy(xs[rank]).to(dev), "sum")

@@ -46,11 +46,19 @@ def host(t):
 NP_TORCH = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
 
 
+@pytest.fixture(params=["pull", "push"])
+def impl(request, monkeypatch):
+    """Both data-movement forms of the all-reduce kernels: pull (K1/K2, the virtual
+    default) and push (K1p/K2p, the multi-process default), selected by RP_AR_IMPL."""
+    monkeypatch.setenv("RP_AR_IMPL", request.param)
+    return request.param
+
+
 # --- all_reduce vs the reference's stitched folds ---------------------------
 
 @pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
 @pytest.mark.parametrize("kind", ["sum", "mean", "max", "premean"])
-def test_all_reduce_matches_reference_folds(folds, algo, kind):
+def test_all_reduce_matches_reference_folds(folds, algo, kind, impl):
     for key, dtype, n, shape in fold_cases(folds):
         xs = [to_dev(folds[f"{key}_in{r}"]).reshape(-1) for r in range(n)]
         want = folds[f"{key}_{kind}"]
@@ -78,7 +86,7 @@ def test_all_gather_and_broadcast_match_reference(folds):
 
 @pytest.mark.parametrize("n", [2, 3, 4, 8])
 @pytest.mark.parametrize("count", [1, 3, 5, 127, 1000, 4097, 65537, 1 << 20])
-def test_all_reduce_sizes_f32(n, count):
+def test_all_reduce_sizes_f32(n, count, impl):
     rng = np.random.default_rng(count * 10 + n)
     xs_np = [rng.standard_normal(count).astype(np.float32) for _ in range(n)]
     for kind in ("sum", "premean", "max"):
@@ -89,7 +97,7 @@ def test_all_reduce_sizes_f32(n, count):
                 assert host(o).tobytes() == want.tobytes(), (kind, algo)
 
 
-def test_all_reduce_misaligned_views():
+def test_all_reduce_misaligned_views(impl):
     n = 4
     rng = np.random.default_rng(9)
     base = [to_dev(rng.standard_normal(10001).astype(np.float32)) for _ in range(n)]
@@ -105,7 +113,7 @@ def test_all_reduce_misaligned_views():
             assert host(ob[:3]).tobytes() == np.zeros(3, np.float32).tobytes()
 
 
-def test_all_reduce_large_f32_premean_8_replicas():
+def test_all_reduce_large_f32_premean_8_replicas(impl):
     # 64 MiB per replica, the north-star message size
     n, count = 8, 16 << 20
     gens = [torch.Generator(device=DEV).manual_seed(1234 + r) for r in range(n)]
@@ -117,9 +125,9 @@ def test_all_reduce_large_f32_premean_8_replicas():
         assert host(o).tobytes() == want.tobytes()
 
 
-def test_staged_in_pieces_when_pool_small():
-    n, count = 4, 3 << 20  # 12 MiB per replica through a 4 MiB pool
-    comm = VirtualCommunicator(n, device=0, pool_bytes=4 << 20)
+def test_staged_in_pieces_when_pool_small(impl):
+    n, count = 4, 12 << 20  # 48 MiB per replica through a 16 MiB pool
+    comm = VirtualCommunicator(n, device=0, pool_bytes=16 << 20)
     rng = np.random.default_rng(11)
     xs_np = [rng.standard_normal(count).astype(np.float32) for _ in range(n)]
     for algo in ("oneshot", "twoshot"):
@@ -133,7 +141,7 @@ def test_staged_in_pieces_when_pool_small():
 # --- bf16 / f16 and the fused exchange cast --------------------------------------
 
 @pytest.mark.parametrize("n", [2, 4, 8])
-def test_bf16_all_reduce_matches_oracle(n):
+def test_bf16_all_reduce_matches_oracle(n, impl):
     rng = np.random.default_rng(20 + n)
     bits = [O.f32_to_bf16_bits(rng.standard_normal(50001).astype(np.float32)) for _ in range(n)]
     xs = [to_dev(b.view(np.int16)).view(torch.bfloat16) for b in bits]
@@ -146,7 +154,7 @@ def test_bf16_all_reduce_matches_oracle(n):
                 assert np.array_equal(got, want), (kind, algo)
 
 
-def test_f32_grads_exchanged_as_bf16():
+def test_f32_grads_exchanged_as_bf16(impl):
     n = 4
     rng = np.random.default_rng(31)
     xs_np = [rng.standard_normal(30011).astype(np.float32) for _ in range(n)]
@@ -169,7 +177,7 @@ def test_f16_all_reduce():
 
 # --- zero-copy pool buffers (in place) ------------------------------------------
 
-def test_pool_in_place_all_reduce_and_gather():
+def test_pool_in_place_all_reduce_and_gather(impl):
     n = 4
     comm = VirtualCommunicator(n, device=0, pool_bytes=32 << 20)
     bufs = comm.alloc(1 << 20, torch.float32)

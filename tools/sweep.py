@@ -32,6 +32,7 @@ def main():
     p.add_argument("--ops", default="all_reduce,all_gather,broadcast")
     p.add_argument("--algos", default="auto,oneshot,twoshot")
     p.add_argument("--iters", type=int, default=20)
+    p.add_argument("--flush", action="store_true", help="flush L2 and time every iteration alone")
     a = p.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -97,18 +98,27 @@ def main():
                     factor = 1.0
                 for _ in range(3):
                     fn()
-                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                       for _ in range(a.iters)]
                 torch.cuda.synchronize()
                 if world > 1:
                     torch.distributed.barrier()
-                for e0, e1 in evs:
-                    flush.zero_()
+                if a.flush:
+                    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                           for _ in range(a.iters)]
+                    for e0, e1 in evs:
+                        flush.zero_()
+                        e0.record(stream)
+                        fn()
+                        e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms = tmax(statistics.median(e0.elapsed_time(e1) for e0, e1 in evs))
+                else:  # nccl-tests convention: back-to-back launches, mean time
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
-                    fn()
+                    for _ in range(a.iters):
+                        fn()
                     e1.record(stream)
-                torch.cuda.synchronize()
-                ms = tmax(statistics.median(e0.elapsed_time(e1) for e0, e1 in evs))
+                    torch.cuda.synchronize()
+                    ms = tmax(e0.elapsed_time(e1) / a.iters)
                 bus = factor * size / (ms / 1e3) / 1e9
                 rows.append({"op": op, "algo": algo, "bytes": size, "n": n, "gpus": world, "us": ms * 1e3,
                              "busbw_gbs": bus})
