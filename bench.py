@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--replicas", type=int, default=8, help="replicas emulated on one GPU when N=1")
     p.add_argument("--kind", default="premean")
     p.add_argument("--algo", default="auto")
+    p.add_argument("--ar-impl", default=None, choices=["push", "pull"],
+                   help="force the all-reduce data-movement form (default: push multi-process, pull virtual)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=10.0)
     p.add_argument("--e2e-steps", type=int, default=10)
@@ -329,6 +331,8 @@ def run_e2e(args, comm, world, n, count, dev, stream):
 
 def main():
     args = parse()
+    if args.ar_impl:
+        os.environ["RP_AR_IMPL"] = args.ar_impl
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))

@@ -214,7 +214,7 @@ def body_timeout(rank, world):
     from paper_1902_00465_b200 import errors
     from paper_1902_00465_b200.comm import Communicator
 
-    comm = Communicator(device=rank, pool_bytes=8 << 20, timeout_s=2.0)
+    comm = Communicator(device=rank, pool_bytes=16 << 20, timeout_s=2.0)
     x = torch.ones(1024, device=f"cuda:{rank}")
     if rank != world - 1:
         comm.all_reduce_tensor(x, "sum")

@@ -355,7 +355,7 @@ def test_wrap_optimizer_matches_reference_bitwise(wrap_golden):
     wrap_golden = {k: wrap_golden[k] for k in wrap_golden.files}  # NpzFile is not thread-safe
     for n in (2, 4):
         nw = len([k for k in wrap_golden if k.startswith(f"small_n{n}_w")])
-        repl = Replicator(num_replicas=n, device=0, pool_bytes=8 << 20)
+        repl = Replicator(num_replicas=n, device=0, pool_bytes=16 << 20)
         with repl.context():
             params = repl.replicate(lambda: torch.nn.ParameterList(
                 [torch.nn.Parameter(to_dev(wrap_golden[f"small_n{n}_w{i}"])) for i in range(nw)]))
@@ -394,7 +394,7 @@ def test_config1_average_md5(wrap_golden):
 
 
 def test_replicator_run_all_sum_and_protocol_error():
-    repl = Replicator(num_replicas=3, device=0, pool_bytes=8 << 20)
+    repl = Replicator(num_replicas=3, device=0, pool_bytes=16 << 20)
 
     def step(x):
         return repl.all_sum(x, label="g")
@@ -413,7 +413,7 @@ def test_replicator_run_all_sum_and_protocol_error():
 
 def test_replicator_paper_batch_norm_kat():
     # h0=[1,3], h1=[5,7] -> (h - 4)/sqrt(5 + eps)
-    repl = Replicator(num_replicas=2, device=0, pool_bytes=8 << 20)
+    repl = Replicator(num_replicas=2, device=0, pool_bytes=16 << 20)
     hs = [torch.tensor([1.0, 3.0], device=DEV, dtype=torch.float64),
           torch.tensor([5.0, 7.0], device=DEV, dtype=torch.float64)]
     outs = repl.run(lambda h: repl.batch_norm(h), lambda r: hs[r])
@@ -424,7 +424,7 @@ def test_replicator_paper_batch_norm_kat():
 
 def test_cross_replica_bn_module_forward_virtual():
     n = 2
-    repl = Replicator(num_replicas=n, device=0, pool_bytes=8 << 20)
+    repl = Replicator(num_replicas=n, device=0, pool_bytes=16 << 20)
     g = torch.Generator(device=DEV).manual_seed(10)
     xs = [torch.randn(4, 16, 3, 3, device=DEV, generator=g) for _ in range(n)]
     bns = repl.replicate(lambda: CrossReplicaBatchNorm(16, repl))
