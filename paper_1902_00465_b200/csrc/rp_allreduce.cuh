@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot(const CollArgs a) {
   const size_t sub = (Vc + gridDim.x - 1) / gridDim.x;
   const size_t b0 = (size_t)blockIdx.x * sub;
   const size_t b1 = std::min(b0 + sub, Vc);
+  rp_trace(a, 0);
 
   if (a.copy_in && b0 < b1) {
     char* mine = a.t.data[rank] + a.read_off;
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot(const CollArgs a) {
     // staging is read after the last barrier above: hold peers until we are done
     rank_barrier(a, rank, blockIdx.x, a.epoch + 3);
   }
+  rp_trace(a, 7);
 }
 
 // Element-type plumbing shared by the push kernels: user src -> exchange T,
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_push(const CollArgs a) {
   const size_t b1 = std::min(b0 + sub, Vc);
   const void* src = a.src[rank];
   const bool ali = aligned16(src);
+  rp_trace(a, 0);
 
   // phase 1: scatter my chunks to their owners (stagger targets across ranks)
 #pragma unroll 1
@@ -319,6 +322,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_push(const CollArgs a) {
     }
     rank_barrier(a, rank, blockIdx.x, a.epoch + 3);
   }
+  rp_trace(a, 7);
 }
 
 // ---------------------------------------------------------------------------

@@ -16,7 +16,10 @@
 // (SPEC.md:188-222).
 #include <stdlib.h>
 
+#include <stdio.h>
+
 #include <algorithm>
+#include <vector>
 
 #include "rp_device.cuh"
 
@@ -194,7 +197,40 @@ void fill_ptrs(rp_comm* c, CollArgs& a, const void* const* src, void* const* dst
   }
 }
 
+// Launch a collective kernel; with RP_TRACE=<file> (analysis only) also collect
+// the per-block %globaltimer stamps (rp_device.cuh rp_trace) and append them as
+// one JSON line per launch. Tracing synchronises the stream.
+int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t stream, const char* tag) {
+  const char* path = getenv("RP_TRACE");
+  const size_t n = (size_t)grid.x * grid.y * 8;
+  unsigned long long* buf = nullptr;
+  a.trace = nullptr;
+  if (path) {
+    RP_CUDA_CHECK(cudaMalloc(&buf, n * 8));
+    RP_CUDA_CHECK(cudaMemsetAsync(buf, 0, n * 8, stream));
+    a.trace = buf;
+  }
+  void* args[] = {&a};
+  const int rc = rp_launch(c, fn, grid, dim3(kThreads), args, 0, stream);
+  if (path) {
+    std::vector<unsigned long long> h(n);
+    cudaStreamSynchronize(stream);
+    cudaMemcpy(h.data(), buf, n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    a.trace = nullptr;
+    if (FILE* f = fopen(path, "a")) {
+      fprintf(f, "{\"tag\":\"%s\",\"rank\":%d,\"world\":%d,\"grid\":[%u,%u],\"count\":%zu,\"stamps\":[", tag, c->rank,
+              c->world, grid.x, grid.y, a.count);
+      for (size_t i = 0; i < n; ++i) fprintf(f, "%s%llu", i ? "," : "", h[i]);
+      fprintf(f, "]}\n");
+      fclose(f);
+    }
+  }
+  return rc;
+}
+
 void base_args(rp_comm* c, CollArgs& a) {
+  a.trace = nullptr;
   a.t = c->table;
   a.world = c->world;
   a.rank = c->is_virtual ? -1 : c->rank;
@@ -254,11 +290,22 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   if (algo != RP_ALGO_ONESHOT && algo != RP_ALGO_TWOSHOT)
     return rp_fail(RP_ERR_INVALID, "all_reduce: unknown algorithm");
 
-  // Data-movement form. Push (only stores cross NVLink, every fold reads local
-  // HBM; measured bidirectional peer STG 690 vs LDG 650 GB/s, tools/nvlink_probe)
-  // for one-process-per-GPU communicators; pull (each buffer read and written
-  // exactly once: the HBM-minimal form) for virtual replicas sharing one GPU.
-  int push = c->is_virtual ? 0 : 1;
+  // Data-movement form (measured): for one-process-per-GPU
+  // communicators the one-shot is the push form (reads src in place, ONE barrier:
+  // 8 us vs 16 us at 1 KiB, N=2); the two-shot is the pull form when the source is
+  // pool-resident (zero-copy: 628 vs 512 GB/s at 256 MiB, N=2) and the push form
+  // when it would need staging (it reads src in place: 465 vs 376 GB/s at 64 MiB).
+  // Virtual replicas share one GPU's HBM: the pull form, which reads and writes
+  // every buffer exactly once. RP_AR_IMPL=push|pull overrides (tests, A/B).
+  int push;
+  if (c->is_virtual) {
+    push = 0;
+  } else if (algo == RP_ALGO_ONESHOT) {
+    push = 1;
+  } else {
+    size_t off0;
+    push = (dtype_in == dtype_comm && symmetric_in_pool(c, src, count * rp_dtype_size(dtype_in), &off0)) ? 0 : 1;
+  }
   if (const char* e = getenv("RP_AR_IMPL")) push = (e[0] == 'p' && e[1] == 'u' && e[2] == 's') ? 1 : 0;
   if (push) return launch_push(c, src, dst, count, dtype_in, dtype_comm, dtype_out, op, algo, stream, a);
 
@@ -340,8 +387,8 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   a.epoch = c->epoch;
   c->epoch += (algo == RP_ALGO_TWOSHOT && a.copy_out) ? 3 : 2;
   c->calls += 1;
-  void* args[] = {&a};
-  return rp_launch(c, fn, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads), args, 0, stream);
+  return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream,
+                     algo == RP_ALGO_TWOSHOT ? "twoshot_pull" : "oneshot_pull");
 }
 
 // Push-form all-reduce (K1p one-shot / K2p two-shot, rp_allreduce.cuh).
@@ -408,8 +455,8 @@ static int launch_push(rp_comm* c, const void* const* src, void* const* dst, siz
   a.epoch = c->epoch;
   c->epoch += epochs;
   c->calls += 1;
-  void* args[] = {&a};
-  return rp_launch(c, fn, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads), args, 0, stream);
+  return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream,
+                     algo == RP_ALGO_TWOSHOT ? "twoshot_push" : "oneshot_push");
 }
 
 // All-gather: rank order (graph.py:575-579). Inputs are read from the peers'

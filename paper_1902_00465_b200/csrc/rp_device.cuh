@@ -103,8 +103,18 @@ __device__ __forceinline__ bool rank_barrier(const RankTable& t, int world, uint
   __syncthreads();
   return s_ok != 0;
 }
+// RP_TRACE analysis stamps: 8 u64 per block -- [0] start, [2k-1]/[2k] enter/leave
+// barrier k (k = 1..3), [7] end.
+__device__ __forceinline__ void rp_trace(const CollArgs& a, int slot) {
+  if (a.trace != nullptr && threadIdx.x == 0)
+    a.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + slot] = globaltimer();
+}
 __device__ __forceinline__ bool rank_barrier(const CollArgs& a, int rank, int row, uint32_t value) {
-  return rank_barrier(a.t, a.world, a.timeout_ns, rank, row, value);
+  const int k = (int)(value - a.epoch);
+  rp_trace(a, 2 * k - 1);
+  const bool ok = rank_barrier(a.t, a.world, a.timeout_ns, rank, row, value);
+  rp_trace(a, 2 * k);
+  return ok;
 }
 
 // ---------------------------------------------------------------------------

@@ -94,6 +94,7 @@ struct CollArgs {
   int root;
   uint32_t epoch;       // barrier values epoch+1, epoch+2, ...
   uint64_t timeout_ns;
+  unsigned long long* trace;  // RP_TRACE analysis: per-block %globaltimer stamps, or NULL
 };
 
 // error plumbing

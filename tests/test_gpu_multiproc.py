@@ -138,6 +138,70 @@ def body_gather_broadcast(rank, world):
     comm.close()
 
 
+class RefTensor:
+    """Stand-in for the reference's Tensor (tensor.py:32-98: immutable f32/f64 array,
+    ``.np``, ``.shape``, ``.dtype``, ``Tensor.wrap``); /root/reference is not on the box."""
+
+    def __init__(self, arr):
+        arr = np.ascontiguousarray(arr)
+        arr.setflags(write=False)
+        self._np = arr
+
+    @staticmethod
+    def wrap(arr):
+        return RefTensor(arr)
+
+    @property
+    def np(self):
+        return self._np
+
+    @property
+    def shape(self):
+        return self._np.shape
+
+    @property
+    def dtype(self):
+        return {np.dtype(np.float32): "f32", np.dtype(np.float64): "f64"}[self._np.dtype]
+
+
+def body_mesh_seam(rank, world):
+    """Replay what the reference's mesh seam hands a communicator
+    (tests/golden/mesh_seam.json, recorded from graph.py:565-583) and check our
+    Communicator returns what the seam expects, as the reference's Tensor type."""
+    import json
+
+    from paper_1902_00465_b200.comm import Communicator
+    from tests.helpers import GOLDEN
+
+    if world != 2:
+        return
+    comm = Communicator(device=rank, pool_bytes=16 << 20)
+    trace = json.load(open(os.path.join(GOLDEN, "mesh_seam.json")))["trace"]
+    for t in trace:
+        if t["rank"] != rank:
+            continue
+        npd = np.float32 if t["dtype"] == "f32" else np.float64
+        shape = tuple(t["calls"][0]["shape"])          # what the seam passes (scalars as (1,))
+        local = RefTensor(np.full(shape, float(rank + 1), npd))
+        outs = []
+        for c in t["calls"]:
+            if c["op"] == "all_reduce":
+                r = comm.all_reduce(local, c["kind"], c["label"])
+                assert isinstance(r, RefTensor) and r.shape == local.shape and r.dtype == t["dtype"]
+                outs.append(r.np)
+            elif c["op"] == "all_gather":
+                parts = comm.all_gather(local, c["label"])
+                assert all(isinstance(p, RefTensor) for p in parts) and len(parts) == 2
+                outs.append(np.concatenate([p.np for p in parts], axis=0))  # graph.py:579
+            else:
+                rv = local if rank == 0 else None
+                r = comm.broadcast(rv, c["label"], shape=tuple(c["shape"]), dtype=c["dtype"])
+                outs.append(r.np)
+        for got, want in zip(outs, t["out_values"]):
+            assert got.reshape(-1).tolist() == want, (t["shape"], t["dtype"])
+    comm.close()
+
+
 def body_bn(rank, world):
     from oracle import collectives as O
     from paper_1902_00465_b200.replicator import CrossReplicaBatchNorm, Replicator
@@ -233,6 +297,10 @@ def test_all_reduce_multiprocess():
 
 def test_gather_broadcast_multiprocess():
     run_world("body_gather_broadcast")
+
+
+def test_reference_mesh_seam_replay():
+    run_world("body_mesh_seam", world=2)
 
 
 def test_cross_replica_bn_autograd_multiprocess():
