@@ -243,6 +243,8 @@ class Communicator(_Base):
         if isinstance(local, torch.Tensor):
             return self.all_reduce_tensor(local, kind, **kw)
         arr, wrap = _host_in(local)
+        if hasattr(local, "np") and hasattr(type(local), "wrap"):
+            self._tensor_cls = type(local)
         x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
         y = self.all_reduce_tensor(x, kind)
         return wrap(y.cpu().numpy())
@@ -266,10 +268,16 @@ class Communicator(_Base):
                  else torch.empty(tuple(shape), dtype=dtype, device=f"cuda:{self.device}"))
             return self.broadcast_tensor(x, root)
         if root_value is None:
+            # non-root ranks hold no value: return the reference's Tensor type if we
+            # have seen it (the seam calls ``.np`` on the result, graph.py:582), else
+            # a read-only HostTensor with the same interface
             np_dt = {"f32": np.float32, "f64": np.float64}.get(dtype, dtype)
-            arr, wrap = np.zeros(tuple(shape), dtype=np_dt), _wrapper_for(None)
+            arr = np.zeros(tuple(shape), dtype=np_dt)
+            wrap = _wrapper_for(None, getattr(self, "_tensor_cls", None))
         else:
             arr, wrap = _host_in(root_value)
+            if hasattr(root_value, "np") and hasattr(type(root_value), "wrap"):
+                self._tensor_cls = type(root_value)
         x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
         y = self.broadcast_tensor(x, root)
         return wrap(y.cpu().numpy())
@@ -396,19 +404,54 @@ def _contig_cuda(x: torch.Tensor, device: int) -> torch.Tensor:
     return x if x.is_contiguous() else x.contiguous()
 
 
-def _wrapper_for(local):
+class HostTensor:
+    """Read-only host result with the reference Tensor's interface (tensor.py:32-98:
+    ``.np``, ``.shape``, ``.dtype`` in {"f32","f64"}, ``wrap``), returned to a non-root
+    broadcast caller that passed no value to infer its Tensor type from."""
+
+    __slots__ = ("_np",)
+
+    def __init__(self, arr):
+        arr = np.ascontiguousarray(arr)
+        arr.setflags(write=False)
+        self._np = arr
+
+    @staticmethod
+    def wrap(arr):
+        return HostTensor(arr)
+
+    @property
+    def np(self):
+        return self._np
+
+    @property
+    def shape(self):
+        return self._np.shape
+
+    @property
+    def dtype(self):
+        return {np.dtype(np.float32): "f32", np.dtype(np.float64): "f64"}[self._np.dtype]
+
+    def tolist(self):
+        return self._np.tolist()
+
+
+def _wrapper_for(local, cls=None):
     """Return a function turning a numpy result back into the caller's value kind:
     the reference Tensor class when given one (``Tensor.wrap``, tensor.py:52-62),
-    else a numpy array."""
+    a numpy array for numpy input, and ``cls`` (or HostTensor) when there is no input."""
     if local is not None and hasattr(local, "np") and hasattr(type(local), "wrap"):
         cls = type(local)
+    elif local is None:
+        cls = cls or HostTensor
+    else:
+        return lambda a: np.ascontiguousarray(a)
 
-        def wrap(a):
-            a = np.ascontiguousarray(a)
-            a.setflags(write=False)
-            return cls.wrap(a)
-        return wrap
-    return lambda a: np.ascontiguousarray(a)
+    def wrap(a):
+        a = np.ascontiguousarray(a)
+        a.setflags(write=False)
+        return cls.wrap(a)
+    return wrap
 
 
 def _host_in(local):

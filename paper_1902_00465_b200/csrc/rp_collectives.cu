@@ -218,7 +218,9 @@ int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t
     cudaMemcpy(h.data(), buf, n * 8, cudaMemcpyDeviceToHost);
     cudaFree(buf);
     a.trace = nullptr;
-    if (FILE* f = fopen(path, "a")) {
+    char fname[1024];
+    snprintf(fname, sizeof(fname), "%s.rank%d", path, c->rank);
+    if (FILE* f = fopen(fname, "a")) {
       fprintf(f, "{\"tag\":\"%s\",\"rank\":%d,\"world\":%d,\"grid\":[%u,%u],\"count\":%zu,\"stamps\":[", tag, c->rank,
               c->world, grid.x, grid.y, a.count);
       for (size_t i = 0; i < n; ++i) fprintf(f, "%s%llu", i ? "," : "", h[i]);

@@ -10,7 +10,8 @@ import sys
 
 
 def main(path, min_count=1 << 20):
-    rows = [json.loads(line) for line in open(path)]
+    import glob
+    rows = [json.loads(line) for p in sorted(glob.glob(path + ".rank*")) for line in open(p)]
     rows = [r for r in rows if r["count"] >= min_count]
     by = {}
     for r in rows:
