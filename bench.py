@@ -197,7 +197,8 @@ def run_ours(args, rank, world, local):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     count = args.bytes // 4
-    pool = args.bytes + (64 << 20)
+    # fusion buffer + a landing region of the same size (push two-shot) + headroom
+    pool = 2 * args.bytes + (64 << 20)
     if world == 1:
         n = args.replicas
         comm = VirtualCommunicator(n, device=local, pool_bytes=pool)

@@ -432,8 +432,18 @@ class HostTensor:
     def dtype(self):
         return {np.dtype(np.float32): "f32", np.dtype(np.float64): "f64"}[self._np.dtype]
 
+    @property
+    def size(self):
+        return self._np.size
+
     def tolist(self):
         return self._np.tolist()
+
+    def tobytes(self):
+        return self._np.tobytes()
+
+    def item(self):
+        return float(self._np.item())
 
 
 def _wrapper_for(local, cls=None):
