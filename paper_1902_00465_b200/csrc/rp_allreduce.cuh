@@ -127,78 +127,6 @@ __device__ __forceinline__ uint4 fold_packet(const uint4 (&x)[NR]) {
   return out.u;
 }
 
-// ---------------------------------------------------------------------------
-// K2: two-shot all-reduce
-// ---------------------------------------------------------------------------
-template <int DT, int OP, int NR>
-__global__ void __launch_bounds__(kThreads) ar_twoshot(const CollArgs a) {
-  using T = typename DType<DT>::T;
-  using A = typename DType<DT>::Acc;
-  const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
-  const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
-  const size_t Vc = a.chunk;
-  const size_t sub = (Vc + gridDim.x - 1) / gridDim.x;
-  const size_t b0 = (size_t)blockIdx.x * sub;
-  const size_t b1 = std::min(b0 + sub, Vc);
-  rp_trace(a, 0);
-
-  if (a.copy_in && b0 < b1) {
-    char* mine = a.t.data[rank] + a.read_off;
-#pragma unroll 1
-    for (int c = 0; c < NR; ++c) {
-      const size_t lo = c * Vc + b0, hi = std::min(c * Vc + b1, V);
-      if (lo < hi) stage_in<T>(a, rank, mine, lo, hi);
-    }
-  }
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
-
-  const char* in[NR];
-  char* out[NR];
-#pragma unroll
-  for (int p = 0; p < NR; ++p) {
-    in[p] = a.t.data[p] + a.read_off;
-    out[p] = a.t.data[p] + a.write_off;
-  }
-  const size_t lo = rank * Vc + b0;
-  const size_t hi = std::min(rank * Vc + b1, V);
-  const size_t stride = (size_t)blockDim.x * kUnroll;
-  for (size_t base = lo + threadIdx.x; base < hi; base += stride) {
-    uint4 x[kUnroll][NR];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const size_t v = base + (size_t)u * blockDim.x;
-      if (v < hi) {
-#pragma unroll
-        for (int p = 0; p < NR; ++p) x[u][p] = ld128(in[p] + v * 16);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const size_t v = base + (size_t)u * blockDim.x;
-      if (v < hi) {
-        const uint4 r = fold_packet<T, A, OP, NR>(x[u]);
-#pragma unroll
-        for (int p = 0; p < NR; ++p) st128(out[p] + v * 16, r);
-      }
-    }
-  }
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 2)) return;
-
-  if (a.copy_out) {
-    if (b0 < b1) {
-      const char* mine = a.t.data[rank] + a.write_off;
-#pragma unroll 1
-      for (int c = 0; c < NR; ++c) {
-        const size_t l = c * Vc + b0, h = std::min(c * Vc + b1, V);
-        if (l < h) stage_out<T>(a, rank, mine, l, h);
-      }
-    }
-    // staging is read after the last barrier above: hold peers until we are done
-    rank_barrier(a, rank, blockIdx.x, a.epoch + 3);
-  }
-  rp_trace(a, 7);
-}
-
 // Element-type plumbing shared by the push kernels: user src -> exchange T,
 // exchange T -> user dst (fused casts, tails and misalignment handled).
 template <typename T>
@@ -219,108 +147,154 @@ __device__ __forceinline__ void store_dst(const CollArgs& a, void* dst, size_t v
   store_user<T>((T*)dst, v, a.count, al, r);
 }
 
+// Claim the next tile of `phase` from this rank's local counter (one atomic per
+// block per tile). Every block ends with exactly one failing claim, so a call
+// advances the counter by ntiles + gridDim.x (host-tracked a.tile_base).
+__device__ __forceinline__ uint32_t claim_tile(const CollArgs& a, int rank, int phase) {
+  __shared__ uint32_t s_tile;
+  __syncthreads();  // everyone has read the previous claim
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + phase, 1u) - a.tile_base[phase];
+  __syncthreads();
+  return s_tile;
+}
+
+// Phase end for the dynamically scheduled kernels: count this block in, wait for
+// every block of every rank (trace slots 2p+1 / 2p+2).
+__device__ __forceinline__ bool phase_end(const CollArgs& a, int rank, int phase) {
+  phase_arrive(a.t, a.world, rank, phase);
+  rp_trace(a, 2 * phase + 1);
+  const bool ok = phase_wait(a.t, a.world, a.timeout_ns, rank, phase, a.ph_target[phase]);
+  rp_trace(a, 2 * phase + 2);
+  return ok;
+}
+
 // ---------------------------------------------------------------------------
-// K2p: two-shot all-reduce, push form (the NVLink path). Only stores cross the
-// links; every reduction reads local HBM.
-//   phase 1: rank r pushes chunk c of its src into rank c's landing slot Q_c[r]
-//   barrier
-//   phase 2: rank r folds chunk r: its own src plus Q_r[p] for p != r, ascending
-//            rank order, and pushes the rounded result into every rank's output
-//            (the pool dst region, or the pool W region when dst is a user buffer)
-//   barrier ; [copy W -> user dst ; barrier]
-// No start barrier: a peer's Q region is only read between that peer's two
-// barriers of the same call (see rp_internal.h pool layout).
-// a.read_off = Q offset (slots of a.chunk vectors per source rank),
-// a.write_off = output offset, a.copy_out = output is W (user dst elsewhere).
+// K2d: two-shot all-reduce, dynamically scheduled (the default large-message
+// kernel, both data-movement forms). Blocks claim tiles of tile_v vectors from a
+// per-rank atomic counter and phases are separated by rank-level counter
+// barriers, so no block waits on one particular peer block and the tail is one
+// tile (static per-block partitioning left a 20-60 us end spread, RP_TRACE).
+//
+// PULL (PUSH = false; src pool-resident, or staged by phase 0):
+//   P0  [copy_in] stage every chunk's tiles of src into pool[read_off]   | barrier 0
+//   P1  tiles of chunk `rank`: load all N operands (N-1 over NVLink), fold in
+//       rank order, store the result into every rank's pool[write_off]   | barrier 1
+//   P2  [copy_out] pool[write_off] -> user dst, all chunks                | barrier 2
+// PUSH (PUSH = true; src anywhere):
+//   P0  tiles of chunks c != rank: src -> Q_c[rank] (stores over NVLink)  | barrier 0
+//   P1  tiles of chunk `rank`: own src + Q_rank[p], fold, store result to
+//       every rank's pool[write_off] (dst region, or W)                   | barrier 1
+//   P2  [copy_out] W -> user dst for chunks c != rank                     | barrier 2
+// Barrier 0 also orders the start: no rank writes into a peer before that peer
+// entered the call (the peer's previous use of its pool is complete).
 // ---------------------------------------------------------------------------
-template <int DT, int OP, int NR>
-__global__ void __launch_bounds__(kThreads) ar_twoshot_push(const CollArgs a) {
+template <int DT, int OP, int NR, bool PUSH>
+__global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
   using T = typename DType<DT>::T;
   using A = typename DType<DT>::Acc;
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
   const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
   const size_t Vc = a.chunk;
-  const size_t sub = (Vc + gridDim.x - 1) / gridDim.x;
-  const size_t b0 = (size_t)blockIdx.x * sub;
-  const size_t b1 = std::min(b0 + sub, Vc);
+  const uint32_t tv = a.tile_v;
+  const uint32_t tpc = (uint32_t)((Vc + tv - 1) / tv);  // tiles per chunk
   const void* src = a.src[rank];
   const bool ali = aligned16(src);
+  void* dst = a.dst[rank];
+  const bool alo = aligned16(dst);
+  // [lo, hi) vectors of tile j of chunk c
+  auto tile_range = [&](int c, uint32_t j, size_t& lo, size_t& hi) {
+    lo = (size_t)c * Vc + (size_t)j * tv;
+    hi = std::min(std::min(lo + tv, (size_t)(c + 1) * Vc), V);
+  };
   rp_trace(a, 0);
 
-  // phase 1: scatter my chunks to their owners (stagger targets across ranks)
-#pragma unroll 1
-  for (int i = 1; i < NR; ++i) {
-    const int c = (rank + i) % NR;
-    const size_t lo = c * Vc + b0, hi = std::min(c * Vc + b1, V);
-    char* slot = a.t.data[c] + a.read_off + (size_t)rank * Vc * 16;  // Q_c[rank]
-    const size_t c0 = c * Vc;
-    constexpr int U = 4;
-    for (size_t base = lo + threadIdx.x; base < hi; base += (size_t)blockDim.x * U) {
-      uint4 x[U];
+  // ---- phase 0 --------------------------------------------------------------
+  if (PUSH) {
+    const uint32_t n0 = tpc * (NR - 1);
+    for (uint32_t i = claim_tile(a, rank, 0); i < n0; i = claim_tile(a, rank, 0)) {
+      const int c = (rank + 1 + (int)(i / tpc)) % NR;
+      size_t lo, hi;
+      tile_range(c, i % tpc, lo, hi);
+      char* slot = a.t.data[c] + a.read_off + ((ptrdiff_t)rank - (ptrdiff_t)c) * (ptrdiff_t)Vc * 16;  // + v*16
+      constexpr int U = 4;
+      for (size_t base = lo + threadIdx.x; base < hi; base += (size_t)blockDim.x * U) {
+        uint4 x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t v = base + (size_t)u * blockDim.x;
-        if (v < hi) x[u] = load_src<T>(a, src, v, ali);
-      }
+        for (int u = 0; u < U; ++u) {
+          const size_t v = base + (size_t)u * blockDim.x;
+          if (v < hi) x[u] = load_src<T>(a, src, v, ali);
+        }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t v = base + (size_t)u * blockDim.x;
-        if (v < hi) st128(slot + (v - c0) * 16, x[u]);
+        for (int u = 0; u < U; ++u) {
+          const size_t v = base + (size_t)u * blockDim.x;
+          if (v < hi) st128(slot + v * 16, x[u]);
+        }
       }
     }
+  } else if (a.copy_in) {
+    const uint32_t n0 = tpc * NR;
+    char* mine = a.t.data[rank] + a.read_off;
+    for (uint32_t i = claim_tile(a, rank, 0); i < n0; i = claim_tile(a, rank, 0)) {
+      size_t lo, hi;
+      tile_range((int)(i / tpc), i % tpc, lo, hi);
+      for (size_t v = lo + threadIdx.x; v < hi; v += blockDim.x) st128(mine + v * 16, load_src<T>(a, src, v, ali));
+    }
   }
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  if (!phase_end(a, rank, 0)) return;
 
-  // phase 2: fold my chunk in rank order, push the result everywhere
+  // ---- phase 1: fold my chunk, store the result on every rank ---------------
   {
-    const size_t lo = rank * Vc + b0, hi = std::min(rank * Vc + b1, V);
-    const char* q = a.t.data[rank] + a.read_off;  // Q_rank[p] at q + (p*Vc + v - rank*Vc)*16
-    const size_t r0 = rank * Vc;
-    void* dst = a.dst[rank];
-    const bool alo = aligned16(dst);
+    const char* in[NR];
+#pragma unroll
+    for (int p = 0; p < NR; ++p) {
+      if (PUSH) in[p] = a.t.data[rank] + a.read_off + ((ptrdiff_t)p - (ptrdiff_t)rank) * (ptrdiff_t)Vc * 16;  // Q_rank[p]
+      else in[p] = a.t.data[p] + a.read_off;
+    }
     constexpr int U = NR > 4 ? 1 : 2;
-    for (size_t base = lo + threadIdx.x; base < hi; base += (size_t)blockDim.x * U) {
-      uint4 x[U][NR];
+    for (uint32_t j = claim_tile(a, rank, 1); j < tpc; j = claim_tile(a, rank, 1)) {
+      size_t lo, hi;
+      tile_range(rank, j, lo, hi);
+      for (size_t base = lo + threadIdx.x; base < hi; base += (size_t)blockDim.x * U) {
+        uint4 x[U][NR];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t v = base + (size_t)u * blockDim.x;
-        if (v < hi) {
+        for (int u = 0; u < U; ++u) {
+          const size_t v = base + (size_t)u * blockDim.x;
+          if (v < hi) {
 #pragma unroll
-          for (int p = 0; p < NR; ++p)
-            x[u][p] = (p == rank) ? load_src<T>(a, src, v, ali) : ld128(q + ((size_t)p * Vc + (v - r0)) * 16);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t v = base + (size_t)u * blockDim.x;
-        if (v < hi) {
-          const uint4 r = fold_packet<T, A, OP, NR>(x[u]);
-#pragma unroll
-          for (int i = 1; i < NR; ++i) {
-            const int p = (rank + i) % NR;
-            st128(a.t.data[p] + a.write_off + v * 16, r);
+            for (int p = 0; p < NR; ++p)
+              x[u][p] = (PUSH && p == rank) ? load_src<T>(a, src, v, ali) : ld128(in[p] + v * 16);
           }
-          if (a.copy_out) store_dst<T>(a, dst, v, alo, r);
-          else st128(a.t.data[rank] + a.write_off + v * 16, r);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t v = base + (size_t)u * blockDim.x;
+          if (v < hi) {
+            const uint4 r = fold_packet<T, A, OP, NR>(x[u]);
+#pragma unroll
+            for (int i = 1; i < NR; ++i) {
+              const int p = (rank + i) % NR;
+              st128(a.t.data[p] + a.write_off + v * 16, r);
+            }
+            if (PUSH && a.copy_out) store_dst<T>(a, dst, v, alo, r);
+            else st128(a.t.data[rank] + a.write_off + v * 16, r);
+          }
         }
       }
     }
   }
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 2)) return;
+  if (!phase_end(a, rank, 1)) return;
 
-  if (a.copy_out) {  // peers' results landed in W: copy them to the user dst
-    if (b0 < b1) {
-      const char* w = a.t.data[rank] + a.write_off;
-      void* dst = a.dst[rank];
-      const bool alo = aligned16(dst);
-#pragma unroll 1
-      for (int c = 0; c < NR; ++c) {
-        if (c == rank) continue;
-        const size_t lo = c * Vc + b0, hi = std::min(c * Vc + b1, V);
-        for (size_t v = lo + threadIdx.x; v < hi; v += blockDim.x) store_dst<T>(a, dst, v, alo, ld128(w + v * 16));
-      }
+  // ---- phase 2: results that landed in staging -> user dst ------------------
+  if (a.copy_out) {
+    const char* w = a.t.data[rank] + a.write_off;
+    const uint32_t n2 = tpc * (PUSH ? NR - 1 : NR);
+    for (uint32_t i = claim_tile(a, rank, 2); i < n2; i = claim_tile(a, rank, 2)) {
+      const int c = PUSH ? (rank + 1 + (int)(i / tpc)) % NR : (int)(i / tpc);
+      size_t lo, hi;
+      tile_range(c, i % tpc, lo, hi);
+      for (size_t v = lo + threadIdx.x; v < hi; v += blockDim.x) store_dst<T>(a, dst, v, alo, ld128(w + v * 16));
     }
-    rank_barrier(a, rank, blockIdx.x, a.epoch + 3);
+    phase_end(a, rank, 2);  // staging is read after barrier 1: hold peers until done
   }
   rp_trace(a, 7);
 }
@@ -459,9 +433,9 @@ const void* pick_ar(int algo, int world, int push) {
   case NR:                                                                                      \
     if (push)                                                                                   \
       return algo == RP_ALGO_ONESHOT ? (const void*)ar_oneshot_push<DT, OP, NR>                 \
-                                     : (const void*)ar_twoshot_push<DT, OP, NR>;                \
+                                     : (const void*)ar_twoshot_dyn<DT, OP, NR, true>;           \
     return algo == RP_ALGO_ONESHOT ? (const void*)ar_oneshot<DT, OP, NR>                        \
-                                   : (const void*)ar_twoshot<DT, OP, NR>;
+                                   : (const void*)ar_twoshot_dyn<DT, OP, NR, false>;
   switch (world) {
     case 1: return (const void*)ar_single<DT, OP>;
     RP_CASE(2) RP_CASE(3) RP_CASE(4) RP_CASE(5) RP_CASE(6) RP_CASE(7) RP_CASE(8)

@@ -231,8 +231,45 @@ int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t
   return rc;
 }
 
+// Launch a dynamically scheduled two-shot (ar_twoshot_dyn): pick the grid and the
+// tile size, hand the kernel its phase-barrier targets and tile-counter bases,
+// and advance the host's copies of those monotone counters (identical on every
+// rank because every quantity here is derived from (count, dtype, world, pool)).
+int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, bool push, const char* tag) {
+  const int W = c->world;
+  const size_t Vc = a.chunk;
+  int blocks = (int)std::min<size_t>((Vc + (size_t)kThreads * 2 - 1) / ((size_t)kThreads * 2), (size_t)RP_MAX_BLOCKS);
+  blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
+  // >= 4 tiles per block so the tail is short; 16..128 KiB tiles, whole warps' worth
+  size_t tv = Vc / ((size_t)blocks * 4);
+  tv = std::min<size_t>(std::max<size_t>(round_up(tv, 512), 1024), 8192);
+  a.tile_v = (uint32_t)tv;
+  const uint32_t tpc = (uint32_t)((Vc + tv - 1) / tv);
+  uint32_t claims[3] = {0, 0, 0};
+  if (push) claims[0] = tpc * (W - 1) + blocks;
+  else if (a.copy_in) claims[0] = tpc * W + blocks;
+  claims[1] = tpc + blocks;
+  if (a.copy_out) claims[2] = tpc * (push ? W - 1 : W) + blocks;
+  const bool used[3] = {true, true, a.copy_out != 0};
+  for (int k = 0; k < 3; ++k) {
+    a.tile_base[k] = c->tile_base[k];
+    a.ph_target[k] = c->ph_base[k] + (uint32_t)blocks;
+  }
+  a.epoch = c->epoch;
+  c->calls += 1;
+  const int rc = launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream, tag);
+  if (rc == RP_OK) {
+    for (int k = 0; k < 3; ++k) {
+      c->tile_base[k] += claims[k];
+      if (used[k]) c->ph_base[k] += (uint32_t)blocks;
+    }
+  }
+  return rc;
+}
+
 void base_args(rp_comm* c, CollArgs& a) {
   a.trace = nullptr;
+  a.tile_v = 0;
   a.t = c->table;
   a.world = c->world;
   a.rank = c->is_virtual ? -1 : c->rank;
@@ -375,22 +412,17 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
 
   const void* fn = pick_ar_any(dtype_comm, op, algo, W, 0);
   if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
-
-  size_t work;  // vectors one rank's blocks cover
   if (algo == RP_ALGO_TWOSHOT) {
     a.chunk = (V + W - 1) / W;
-    work = a.chunk;
-  } else {
-    work = V;
+    return dyn_launch(c, fn, a, stream, false, "twoshot_pull");
   }
   const size_t per_block = (size_t)kThreads * 2;
-  int blocks = (int)std::min<size_t>((work + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
+  int blocks = (int)std::min<size_t>((V + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
   blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
   a.epoch = c->epoch;
-  c->epoch += (algo == RP_ALGO_TWOSHOT && a.copy_out) ? 3 : 2;
+  c->epoch += 2;
   c->calls += 1;
-  return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream,
-                     algo == RP_ALGO_TWOSHOT ? "twoshot_pull" : "oneshot_pull");
+  return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream, "oneshot_pull");
 }
 
 // Push-form all-reduce (K1p one-shot / K2p two-shot, rp_allreduce.cuh).
@@ -445,8 +477,11 @@ static int launch_push(rp_comm* c, const void* const* src, void* const* dst, siz
     a.read_off = scratch;
     a.write_off = dst_pool ? dst_off : scratch + qbytes;
     a.copy_out = dst_pool ? 0 : 1;
-    work = Vc;
-    epochs = dst_pool ? 2 : 3;
+    a.copy_in = 0;
+    a.count = count;
+    const void* fn = pick_ar_any(dtype_comm, op, algo, W, 1);
+    if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
+    return dyn_launch(c, fn, a, stream, true, "twoshot_push");
   }
   a.count = count;
   const void* fn = pick_ar_any(dtype_comm, op, algo, W, 1);

@@ -68,6 +68,35 @@ __device__ __forceinline__ void st128(void* p, uint4 v) {
 // semantics, then spins (acquire) until its own slot (row, p) reaches `value`.
 // Values are monotone per slot, so "reached" is a wrap-safe >= test.
 // Returns false if the wait timed out or a peer aborted (the block must bail).
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Spin (acquire) until *p reaches `target` (wrap-safe >=). Bounded by %globaltimer:
+// on timeout the abort word of every rank is set; a set abort word ends the wait.
+// Returns false on abort/timeout.
+__device__ __forceinline__ bool wait_reach(const RankTable& t, int world, uint64_t timeout_ns, int rank,
+                                           const uint32_t* p, uint32_t target) {
+  uint32_t* abort_word = t.sig[rank] + RP_ABORT_WORD;
+  uint64_t t0 = 0;
+  uint32_t spins = 0;
+  while ((int32_t)(ld_acquire_sys(p) - target) < 0) {
+    if ((++spins & 255u) == 0) {
+      if (ld_relaxed_sys(abort_word) != 0) return false;  // a peer gave up: leave quickly
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > timeout_ns) {
+        // record the timeout locally and tell every peer to stop waiting
+        atomicCAS(abort_word, 0u, RP_ABORT_TIMEOUT);
+        for (int q = 0; q < world; ++q)
+          if (q != rank) atomicCAS(t.sig[q] + RP_ABORT_WORD, 0u, RP_ABORT_PEER);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
 __device__ __forceinline__ bool rank_barrier(const RankTable& t, int world, uint64_t timeout_ns, int rank,
                                              int row, uint32_t value) {
   __shared__ int s_ok;
@@ -77,29 +106,31 @@ __device__ __forceinline__ bool rank_barrier(const RankTable& t, int world, uint
   if (threadIdx.x < (unsigned)world) {
     const int p = threadIdx.x;
     st_release_sys(t.sig[p] + (size_t)row * RP_MAX_RANKS + rank, value);
-    const uint32_t* mine = t.sig[rank] + (size_t)row * RP_MAX_RANKS + p;
-    uint32_t* abort_word = t.sig[rank] + RP_ABORT_WORD;
-    uint64_t t0 = 0;
-    uint32_t spins = 0;
-    while ((int32_t)(ld_acquire_sys(mine) - value) < 0) {
-      if ((++spins & 255u) == 0) {
-        if (ld_relaxed_sys(abort_word) != 0) {  // a peer gave up: leave quickly
-          s_ok = 0;
-          break;
-        }
-        uint64_t now = globaltimer();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > timeout_ns) {
-          // record the timeout locally and tell every peer to stop waiting
-          atomicCAS(abort_word, 0u, RP_ABORT_TIMEOUT);
-          for (int q = 0; q < world; ++q)
-            if (q != rank) atomicCAS(t.sig[q] + RP_ABORT_WORD, 0u, RP_ABORT_PEER);
-          s_ok = 0;
-          break;
-        }
-      }
-    }
+    if (!wait_reach(t, world, timeout_ns, rank, t.sig[rank] + (size_t)row * RP_MAX_RANKS + p, value)) s_ok = 0;
   }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// Rank-level phase barrier for dynamically scheduled kernels (any block may have
+// touched any tile, so every block of every rank must be counted). Arrive: each
+// block adds 1 to counter [phase row][rank] on every rank (release). Wait: every
+// block spins until its own counters [phase row][p] reach `target` (cumulative
+// number of blocks rank p has sent through this phase row, tracked by the host).
+__device__ __forceinline__ void phase_arrive(const RankTable& t, int world, int rank, int phase) {
+  __syncthreads();  // the block's writes happen-before the release
+  if (threadIdx.x < (unsigned)world)
+    red_release_sys_add(t.sig[threadIdx.x] + (size_t)(RP_PH_ROW0 + phase) * RP_MAX_RANKS + rank, 1u);
+}
+__device__ __forceinline__ bool phase_wait(const RankTable& t, int world, uint64_t timeout_ns, int rank, int phase,
+                                           uint32_t target) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < (unsigned)world &&
+      !wait_reach(t, world, timeout_ns, rank, t.sig[rank] + (size_t)(RP_PH_ROW0 + phase) * RP_MAX_RANKS + threadIdx.x,
+                  target))
+    s_ok = 0;
   __syncthreads();
   return s_ok != 0;
 }

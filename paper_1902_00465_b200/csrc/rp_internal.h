@@ -16,7 +16,12 @@
 #define RP_MAX_BLOCKS 1024
 #define RP_BN_ROW0 (RP_MAX_BLOCKS)
 #define RP_BN_ROWS 256
-#define RP_ABORT_WORD ((RP_MAX_BLOCKS + RP_BN_ROWS + 8) * RP_MAX_RANKS)  // u32 index
+// rank-level phase counters of the dynamically scheduled kernels, and the
+// per-rank tile-claim counters (local atomics), one per phase
+#define RP_PH_ROW0 (RP_BN_ROW0 + RP_BN_ROWS)
+#define RP_PH_ROWS 4
+#define RP_CTR_ROW (RP_PH_ROW0 + RP_PH_ROWS)
+#define RP_ABORT_WORD ((RP_CTR_ROW + 4) * RP_MAX_RANKS)  // u32 index
 #define RP_SIGNAL_BYTES (64 * 1024)  // signal region ahead of the data
 #define RP_ALIGN 256
 // Pool layout (every rank identical):
@@ -61,6 +66,10 @@ struct rp_comm {
   double* bn_partials = nullptr;
   size_t bn_partials_bytes = 0;
   uint32_t calls = 0;      // collective calls issued (one-shot landing-zone parity)
+  // dynamically scheduled kernels: cumulative blocks through each phase row (per
+  // source rank; identical on every rank) and cumulative tiles claimed per phase
+  uint32_t ph_base[RP_PH_ROWS] = {};
+  uint32_t tile_base[RP_PH_ROWS] = {};
   // end of the general staging window (see the layout above)
   size_t scratch_end() const { return pool_bytes - RP_BN_BYTES - 2 * RP_OS_REGION; }
   size_t oneshot_zone(int parity) const { return scratch_end() + (size_t)parity * RP_OS_REGION; }
@@ -95,6 +104,10 @@ struct CollArgs {
   uint32_t epoch;       // barrier values epoch+1, epoch+2, ...
   uint64_t timeout_ns;
   unsigned long long* trace;  // RP_TRACE analysis: per-block %globaltimer stamps, or NULL
+  // dynamically scheduled kernels
+  uint32_t tile_v;            // vectors (16 B) per tile
+  uint32_t ph_target[3];      // phase_wait targets (host-tracked cumulative block counts)
+  uint32_t tile_base[3];      // tile-claim counter values at the start of this call
 };
 
 // error plumbing
