@@ -73,84 +73,103 @@ __device__ __forceinline__ void reduce_rows_y(double (&v)[NV], double* smem) {
   }
 }
 
+// NV elements of T starting at p (16-byte vector when NV*sizeof(T) == 16)
+template <typename T, int NV>
+__device__ __forceinline__ void load_nv(const T* p, double (&out)[NV]) {
+  if constexpr (NV * sizeof(T) == 16) {
+    Pack16<T> v;
+    v.u = ld128_stream(p);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = (double)to_acc(v.e[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = (double)to_acc(p[k]);
+  }
+}
+
 // --- NHWC / NC: x is [rows, C], channels innermost ---------------------------
-// block (32, 8): threadIdx.x -> VEC consecutive channels, threadIdx.y -> rows.
-template <typename T, bool BWD>
+// 1-D block of 256 threads over a column block of up to 256 channel-vectors (NV
+// channels each): thread t owns channel-vector t % CVB and rows t / CVB + k*RY
+// (RY = 256 / CVB rows per sweep), so narrow layers (C = 64) still keep every
+// thread busy. U rows are loaded before any is accumulated (U x 16 B in flight
+// per thread), accumulation is f64, and the RY row-partials of a channel are
+// folded in a fixed order through shared memory.
+template <typename T, bool BWD, int NV>
 __global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
-  constexpr int VEC = 16 / sizeof(T);
+  constexpr int U = 4;
   extern __shared__ double smem[];
   const int rep = blockIdx.z;
   const T* x = (const T*)a.x[rep];
   const T* dy = BWD ? (const T*)a.dy[rep] : nullptr;
   const int64_t C = a.C, M = a.rows;
-  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  const int64_t CVt = C / NV;
+  const int64_t cvb0 = (int64_t)blockIdx.x * kBnThreads;
+  const int CVB = (int)std::min<int64_t>(CVt - cvb0, kBnThreads);
+  const int RY = kBnThreads / CVB;
+  const int t = threadIdx.x;
+  const int cv = t % CVB, ry = t / CVB;
+  const bool active = ry < RY;
+  const int64_t c0 = (cvb0 + cv) * NV;
   const int64_t rps = (M + a.S - 1) / a.S;
   const int64_t r0 = (int64_t)blockIdx.y * rps, r1 = std::min(r0 + rps, M);
-  double s1[VEC], s2[VEC], mu[VEC];
+  double s1[NV], s2[NV], mu[NV];
 #pragma unroll
-  for (int k = 0; k < VEC; ++k) {
+  for (int k = 0; k < NV; ++k) {
     s1[k] = 0.0;
     s2[k] = 0.0;
-    mu[k] = (BWD && c0 + k < C) ? (double)a.mean[rep][c0 + k] : 0.0;
+    mu[k] = BWD ? (double)a.mean[rep][c0 + k] : 0.0;
   }
-  const bool full = c0 + VEC <= C;
-  const bool vec = full && (C % VEC == 0) && ((((uintptr_t)x) & 15u) == 0) &&
-                   (!BWD || ((((uintptr_t)dy) & 15u) == 0));
-  if (c0 < C) {
-    for (int64_t r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
-      const int64_t base = r * C + c0;
-      if (vec) {
-        Pack16<T> px;
-        px.u = ld128_stream(x + base);
-        if (BWD) {
-          Pack16<T> pd;
-          pd.u = ld128_stream(dy + base);
+  if (active) {
+    const int64_t step = (int64_t)RY * U;
+    for (int64_t r = r0 + ry; r < r1; r += step) {
+      double xv[U][NV], dv[U][NV];
 #pragma unroll
-          for (int k = 0; k < VEC; ++k) {
-            const double d = (double)to_acc(pd.e[k]);
-            s1[k] += d;
-            s2[k] = fma(d, (double)to_acc(px.e[k]) - mu[k], s2[k]);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < VEC; ++k) {
-            const double v = (double)to_acc(px.e[k]);
-            s1[k] += v;
-            s2[k] = fma(v, v, s2[k]);
-          }
+      for (int u = 0; u < U; ++u) {
+        const int64_t rr = r + (int64_t)u * RY;
+        if (rr < r1) {
+          load_nv<T, NV>(x + rr * C + c0, xv[u]);
+          if (BWD) load_nv<T, NV>(dy + rr * C + c0, dv[u]);
         }
-      } else {
+      }
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-          if (c0 + k >= C) break;
-          const double v = ld_as_f64(x + base + k);
-          if (BWD) {
-            const double d = ld_as_f64(dy + base + k);
-            s1[k] += d;
-            s2[k] = fma(d, v - mu[k], s2[k]);
-          } else {
-            s1[k] += v;
-            s2[k] = fma(v, v, s2[k]);
+      for (int u = 0; u < U; ++u) {
+        if (r + (int64_t)u * RY < r1) {
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            if (BWD) {
+              s1[k] += dv[u][k];
+              s2[k] = fma(dv[u][k], xv[u][k] - mu[k], s2[k]);
+            } else {
+              s1[k] += xv[u][k];
+              s2[k] = fma(xv[u][k], xv[u][k], s2[k]);
+            }
           }
         }
       }
     }
   }
-  double v[2 * VEC];
+  // fold the RY row-partials of each channel-vector in row-group order
+  if (active) {
 #pragma unroll
-  for (int k = 0; k < VEC; ++k) {
-    v[2 * k] = s1[k];
-    v[2 * k + 1] = s2[k];
+    for (int k = 0; k < NV; ++k) {
+      smem[((size_t)ry * CVB + cv) * 2 * NV + 2 * k] = s1[k];
+      smem[((size_t)ry * CVB + cv) * 2 * NV + 2 * k + 1] = s2[k];
+    }
   }
-  reduce_rows_y<2 * VEC>(v, smem);
-  if (threadIdx.y == 0 && c0 < C) {
+  __syncthreads();
+  if (ry == 0) {
+    for (int y = 1; y < RY; ++y)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        s1[k] += smem[((size_t)y * CVB + cv) * 2 * NV + 2 * k];
+        s2[k] += smem[((size_t)y * CVB + cv) * 2 * NV + 2 * k + 1];
+      }
     double* P = a.part[rep] + ((int64_t)blockIdx.y * C) * 2;
 #pragma unroll
-    for (int k = 0; k < VEC; ++k)
-      if (c0 + k < C) {
-        P[(c0 + k) * 2] = v[2 * k];
-        P[(c0 + k) * 2 + 1] = v[2 * k + 1];
-      }
+    for (int k = 0; k < NV; ++k) {
+      P[(c0 + k) * 2] = s1[k];
+      P[(c0 + k) * 2 + 1] = s2[k];
+    }
   }
 }
 
@@ -175,6 +194,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nchw(const BnArgs a) {
   for (int64_t n = n0 + warp; n < n1; n += nwarps) {
     const int64_t base = (n * C + c) * HW;
     if (vec) {
+#pragma unroll 4
       for (int64_t j = (int64_t)lane * VEC; j < HW; j += 32 * VEC) {
         Pack16<T> px;
         px.u = ld128_stream(x + base + j);
@@ -306,37 +326,50 @@ __global__ void __launch_bounds__(kBnThreads) bn_apply_kernel(const T* __restric
   };
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (vec) {
+    constexpr int U = 4;  // U independent 16-byte loads in flight per thread
     const int64_t nv = total / VEC;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
-      const int64_t i0 = v * VEC;
-      Pack16<T> px, pd, py;
-      px.u = ld128_stream(x + i0);
-      if (BWD) pd.u = ld128_stream(dy + i0);
-      if (nchw) {
-        float m, s, k1, k2;
-        coef((i0 / hw) % C, m, s, k1, k2);
+    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < nv; v0 += stride * U) {
+      Pack16<T> px[U], pd[U];
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-          const float xv = to_acc(px.e[k]);
-          float r;
-          if (BWD) r = (to_acc(pd.e[k]) - k1 - (xv - m) * k2) * s;
-          else r = (xv - m) * k1 + k2;
-          py.e[k] = from_f32<T>(r);
-        }
-      } else {
-        const int64_t c0 = i0 % C;
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-          float m, s, k1, k2;
-          coef(c0 + k, m, s, k1, k2);
-          const float xv = to_acc(px.e[k]);
-          float r;
-          if (BWD) r = (to_acc(pd.e[k]) - k1 - (xv - m) * k2) * s;
-          else r = (xv - m) * k1 + k2;
-          py.e[k] = from_f32<T>(r);
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + u * stride;
+        if (v < nv) {
+          px[u].u = ld128_stream(x + v * VEC);
+          if (BWD) pd[u].u = ld128_stream(dy + v * VEC);
         }
       }
-      st128(y + i0, py.u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + u * stride;
+        if (v >= nv) break;
+        const int64_t i0 = v * VEC;
+        Pack16<T> py;
+        if (nchw) {
+          float m, s, k1, k2;
+          coef((i0 / hw) % C, m, s, k1, k2);
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            const float xv = to_acc(px[u].e[k]);
+            float r;
+            if (BWD) r = (to_acc(pd[u].e[k]) - k1 - (xv - m) * k2) * s;
+            else r = (xv - m) * k1 + k2;
+            py.e[k] = from_f32<T>(r);
+          }
+        } else {
+          const int64_t c0 = i0 % C;
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            float m, s, k1, k2;
+            coef(c0 + k, m, s, k1, k2);
+            const float xv = to_acc(px[u].e[k]);
+            float r;
+            if (BWD) r = (to_acc(pd[u].e[k]) - k1 - (xv - m) * k2) * s;
+            else r = (xv - m) * k1 + k2;
+            py.e[k] = from_f32<T>(r);
+          }
+        }
+        st128(y + i0, py.u);
+      }
     }
   } else {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -371,11 +404,17 @@ int ensure_partials(rp_comm* c, size_t bytes) {
   return RP_OK;
 }
 
+// NHWC kernels come in a 16-byte-vector form (NV = 16/sizeof(T); C % NV == 0 and
+// aligned pointers) and a scalar form (NV = 1).
 template <bool BWD>
-const void* pick_partial(int dtype, int layout) {
+const void* pick_partial(int dtype, int layout, bool vec) {
   const bool nchw = layout == RP_LAYOUT_NCHW;
-#define RP_B(DT, T) \
-  if (dtype == DT) return nchw ? (const void*)bn_partial_nchw<T, BWD> : (const void*)bn_partial_nhwc<T, BWD>;
+#define RP_B(DT, T)                                                                    \
+  if (dtype == DT) {                                                                   \
+    if (nchw) return (const void*)bn_partial_nchw<T, BWD>;                              \
+    return vec ? (const void*)bn_partial_nhwc<T, BWD, 16 / sizeof(T)>                  \
+               : (const void*)bn_partial_nhwc<T, BWD, 1>;                              \
+  }
   RP_B(RP_F32, float)
   RP_B(RP_BF16, __nv_bfloat16)
   RP_B(RP_F16, __half)
@@ -391,12 +430,20 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   if (ch > (int64_t)RP_BN_ROWS * kExThreads) return rp_fail(RP_ERR_INVALID, "bn: too many channels (max 65536)");
   if (layout != RP_LAYOUT_NHWC && layout != RP_LAYOUT_NCHW) return rp_fail(RP_ERR_INVALID, "bn: unknown layout");
   if (layout == RP_LAYOUT_NHWC && hw != 1) return rp_fail(RP_ERR_INVALID, "bn: NHWC/NC layout takes hw == 1");
-  const void* fn = bwd ? pick_partial<true>(dtype, layout) : pick_partial<false>(dtype, layout);
-  if (!fn) return rp_fail(RP_ERR_INVALID, "bn: unsupported dtype");
+  if (!rp_dtype_valid(dtype)) return rp_fail(RP_ERR_INVALID, "bn: unsupported dtype");
   const int W = c->world;
   const int nrep = c->is_virtual ? W : 1;
   const size_t esz = rp_dtype_size(dtype);
   const int vec = (int)(16 / esz);
+  bool vecok = (ch % vec) == 0;
+  for (int i = 0; i < nrep; ++i) {
+    const void* xi = c->is_virtual ? ((const void* const*)x)[i] : x;
+    const void* di = bwd ? (c->is_virtual ? ((const void* const*)dy)[i] : dy) : nullptr;
+    vecok = vecok && ((uintptr_t)xi % 16 == 0) && (!bwd || (uintptr_t)di % 16 == 0);
+  }
+  const int nv = vecok ? vec : 1;
+  const void* fn = bwd ? pick_partial<true>(dtype, layout, vecok) : pick_partial<false>(dtype, layout, vecok);
+  if (!fn) return rp_fail(RP_ERR_INVALID, "bn: unsupported dtype");
 
   BnArgs a;
   memset(&a, 0, sizeof(a));
@@ -413,14 +460,17 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   }
   dim3 grid, block;
   size_t smem = 0;
-  const int target = 4 * c->num_sms;
+  const int target = 8 * c->num_sms;
   if (layout == RP_LAYOUT_NHWC) {
-    block = dim3(32, kBnThreads / 32);
-    const int cb = (int)((ch + 32LL * vec - 1) / (32LL * vec));
-    int S = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, (target + cb - 1) / cb));
+    block = dim3(kBnThreads);
+    const int64_t cvt = ch / nv;  // channel-vectors per row
+    const int cb = (int)((cvt + kBnThreads - 1) / kBnThreads);
+    const int64_t ry = kBnThreads / std::min<int64_t>(cvt, kBnThreads);  // rows per sweep
+    int S = (int)std::max<int64_t>(1, std::min<int64_t>((rows + ry * 16 - 1) / (ry * 16), (target + cb - 1) / cb));
+    S = std::min(S, 65535);
     a.S = S;
     grid = dim3(cb, S, nrep);
-    smem = (size_t)kBnThreads * 2 * vec * sizeof(double);
+    smem = (size_t)kBnThreads * 2 * nv * sizeof(double);
   } else {
     block = dim3(kBnThreads);
     int S = (int)std::max<int64_t>(1, std::min<int64_t>(rows, (target + ch - 1) / ch));
