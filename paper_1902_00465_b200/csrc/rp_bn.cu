@@ -43,6 +43,7 @@ struct ExArgs {
   double* count[RP_MAX_RANKS];
   size_t bn_off;  // pool offset of the BN records
   int64_t C;
+  int cpb;        // channels per exchange block (power of two, 1..256)
   double local_count[RP_MAX_RANKS];
   int S;
   int world;
@@ -252,17 +253,38 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nchw(const BnArgs a) {
 }
 
 // --- exchange: fold splits, publish, fold ranks ------------------------------
+// Block = a.cpb channels x (256 / cpb) threads per channel: thread j of a channel
+// folds splits j, j+tpc, ... (independent accumulators, fixed assignment), the tpc
+// partial sums are then folded in lane order through shared memory -- a
+// deterministic order, parallel over the S split partials (a serial loop over S at
+// L2 latency dominated small layers).
 __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
+  __shared__ double red[kExThreads][2];
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
   const int rep = a.rank >= 0 ? 0 : rank;  // local replica index
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int tpc = kExThreads / a.cpb;      // threads per channel
+  const int lane = threadIdx.x % tpc;
+  const int64_t c = (int64_t)blockIdx.x * a.cpb + threadIdx.x / tpc;
   const int64_t C = a.C;
-  if (c < C) {
-    const double* P = a.part[rep];
+  {
     double s1 = 0.0, s2 = 0.0;
-    for (int s = 0; s < a.S; ++s) {
-      s1 += P[((int64_t)s * C + c) * 2];
-      s2 += P[((int64_t)s * C + c) * 2 + 1];
+    if (c < C) {
+      const double* P = a.part[rep];
+#pragma unroll 4
+      for (int s = lane; s < a.S; s += tpc) {
+        s1 += P[((int64_t)s * C + c) * 2];
+        s2 += P[((int64_t)s * C + c) * 2 + 1];
+      }
+    }
+    red[threadIdx.x][0] = s1;
+    red[threadIdx.x][1] = s2;
+  }
+  __syncthreads();
+  if (lane == 0 && c < C) {
+    double s1 = red[threadIdx.x][0], s2 = red[threadIdx.x][1];
+    for (int j = 1; j < tpc; ++j) {
+      s1 += red[threadIdx.x + j][0];
+      s2 += red[threadIdx.x + j][1];
     }
     if (a.bwd) {  // this replica's own sums (weight / bias gradients)
       if (a.out2[rep]) a.out2[rep][c] = (float)s1;
@@ -274,7 +296,7 @@ __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
     rec[2] = a.local_count[rep];
   }
   if (!rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, a.epoch + 1)) return;
-  if (c < C) {
+  if (lane == 0 && c < C) {
     double A1 = 0.0, A2 = 0.0, Mt = 0.0;
     for (int p = 0; p < a.world; ++p) {  // ascending rank order
       const double* rec = (const double*)(a.t.data[p] + a.bn_off) + c * 3;
@@ -460,7 +482,7 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   }
   dim3 grid, block;
   size_t smem = 0;
-  const int target = 8 * c->num_sms;
+  const int target = 3 * c->num_sms;  // ~resident blocks: enough bytes in flight, few split partials
   if (layout == RP_LAYOUT_NHWC) {
     block = dim3(kBnThreads);
     const int64_t cvt = ch / nv;  // channel-vectors per row
@@ -520,7 +542,14 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
       e.count[i] = count;
     }
   }
-  const int blocks = (int)((ch + kExThreads - 1) / kExThreads);
+  // exchange geometry: as many blocks as the BN signal rows and co-residency allow,
+  // >= 16 channels per block, the rest of the 256 threads fold split partials
+  const int max_blocks = std::min(RP_BN_ROWS, rp_blocks_per_rank(c, (const void*)bn_exchange, kExThreads, RP_BN_ROWS));
+  int cpb = 16;
+  while (cpb < kExThreads && (ch + cpb - 1) / cpb > max_blocks) cpb *= 2;
+  e.cpb = cpb;
+  const int blocks = (int)((ch + cpb - 1) / cpb);
+  if (blocks > max_blocks) return rp_fail(RP_ERR_INVALID, "bn: too many channels for the exchange");
   e.epoch = c->epoch;
   c->epoch += 2;
   void* args[] = {&e};
