@@ -97,7 +97,10 @@ __device__ __forceinline__ void load_nv(const T* p, double (&out)[NV]) {
 // folded in a fixed order through shared memory.
 template <typename T, bool BWD, int NV>
 __global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
-  constexpr int U = 4;
+  // raw 16-byte packets stay in registers until accumulated (4 regs per packet),
+  // so 8 rows per thread can be in flight without spilling
+  constexpr bool kPacked = NV * sizeof(T) == 16;
+  constexpr int U = kPacked ? (BWD ? 4 : 8) : 4;
   extern __shared__ double smem[];
   const int rep = blockIdx.z;
   const T* x = (const T*)a.x[rep];
@@ -120,7 +123,40 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
     s2[k] = 0.0;
     mu[k] = BWD ? (double)a.mean[rep][c0 + k] : 0.0;
   }
-  if (active) {
+  if (active && kPacked) {
+    const int64_t step = (int64_t)RY * U;
+    for (int64_t r = r0 + ry; r < r1; r += step) {
+      uint4 px[U], pd[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t rr = r + (int64_t)u * RY;
+        if (rr < r1) {
+          px[u] = ld128_stream(x + rr * C + c0);
+          if (BWD) pd[u] = ld128_stream(dy + rr * C + c0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r + (int64_t)u * RY < r1) {
+          Pack16<T> vx, vd;
+          vx.u = px[u];
+          if (BWD) vd.u = pd[u];
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            const double xk = (double)to_acc(vx.e[k]);
+            if (BWD) {
+              const double dk = (double)to_acc(vd.e[k]);
+              s1[k] += dk;
+              s2[k] = fma(dk, xk - mu[k], s2[k]);
+            } else {
+              s1[k] += xk;
+              s2[k] = fma(xk, xk, s2[k]);
+            }
+          }
+        }
+      }
+    }
+  } else if (active) {
     const int64_t step = (int64_t)RY * U;
     for (int64_t r = r0 + ry; r < r1; r += step) {
       double xv[U][NV], dv[U][NV];
