@@ -147,15 +147,16 @@ __device__ __forceinline__ void store_dst(const CollArgs& a, void* dst, size_t v
   store_user<T>((T*)dst, v, a.count, al, r);
 }
 
-// Claim the next tile of `phase` from this rank's local counter (one atomic per
-// block per tile). Every block ends with exactly one failing claim, so a call
-// advances the counter by ntiles + gridDim.x (host-tracked a.tile_base).
+// Claim the next tile of `phase` from this rank's local counter: one atomic per
+// WARP per tile, broadcast by shuffle -- no block-wide barrier in the main loop
+// (per-block claims cost two __syncthreads per tile: ~1/3 of the stall samples,
+// profiles/r01_ncu_ar_twoshot_dyn_n1.txt). Every warp ends with exactly one failing
+// claim, so a call advances the counter by ntiles + warps (host-tracked tile_base).
 __device__ __forceinline__ uint32_t claim_tile(const CollArgs& a, int rank, int phase) {
-  __shared__ uint32_t s_tile;
-  __syncthreads();  // everyone has read the previous claim
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + phase, 1u) - a.tile_base[phase];
-  __syncthreads();
-  return s_tile;
+  uint32_t t = 0;
+  if ((threadIdx.x & 31) == 0)
+    t = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + phase, 1u) - a.tile_base[phase];
+  return __shfl_sync(0xffffffffu, t, 0);
 }
 
 // Phase end for the dynamically scheduled kernels: count this block in, wait for
@@ -170,7 +171,7 @@ __device__ __forceinline__ bool phase_end(const CollArgs& a, int rank, int phase
 
 // ---------------------------------------------------------------------------
 // K2d: two-shot all-reduce, dynamically scheduled (the default large-message
-// kernel, both data-movement forms). Blocks claim tiles of tile_v vectors from a
+// kernel, both data-movement forms). Warps claim tiles of tile_v vectors from a
 // per-rank atomic counter and phases are separated by rank-level counter
 // barriers, so no block waits on one particular peer block and the tail is one
 // tile (static per-block partitioning left a 20-60 us end spread, RP_TRACE).
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
     hi = std::min(std::min(lo + tv, (size_t)(c + 1) * Vc), V);
   };
   rp_trace(a, 0);
+  const int lane = threadIdx.x & 31;
 
   // ---- phase 0 --------------------------------------------------------------
   if (PUSH) {
@@ -217,16 +219,16 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
       tile_range(c, i % tpc, lo, hi);
       char* slot = a.t.data[c] + a.read_off + ((ptrdiff_t)rank - (ptrdiff_t)c) * (ptrdiff_t)Vc * 16;  // + v*16
       constexpr int U = 4;
-      for (size_t base = lo + threadIdx.x; base < hi; base += (size_t)blockDim.x * U) {
+      for (size_t base = lo + lane; base < hi; base += 32 * U) {
         uint4 x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const size_t v = base + (size_t)u * blockDim.x;
+          const size_t v = base + (size_t)u * 32;
           if (v < hi) x[u] = load_src<T>(a, src, v, ali);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const size_t v = base + (size_t)u * blockDim.x;
+          const size_t v = base + (size_t)u * 32;
           if (v < hi) st128(slot + v * 16, x[u]);
         }
       }
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
     for (uint32_t i = claim_tile(a, rank, 0); i < n0; i = claim_tile(a, rank, 0)) {
       size_t lo, hi;
       tile_range((int)(i / tpc), i % tpc, lo, hi);
-      for (size_t v = lo + threadIdx.x; v < hi; v += blockDim.x) st128(mine + v * 16, load_src<T>(a, src, v, ali));
+      for (size_t v = lo + lane; v < hi; v += 32) st128(mine + v * 16, load_src<T>(a, src, v, ali));
     }
   }
   if (!phase_end(a, rank, 0)) return;
@@ -254,11 +256,11 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
     for (uint32_t j = claim_tile(a, rank, 1); j < tpc; j = claim_tile(a, rank, 1)) {
       size_t lo, hi;
       tile_range(rank, j, lo, hi);
-      for (size_t base = lo + threadIdx.x; base < hi; base += (size_t)blockDim.x * U) {
+      for (size_t base = lo + lane; base < hi; base += 32 * U) {
         uint4 x[U][NR];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const size_t v = base + (size_t)u * blockDim.x;
+          const size_t v = base + (size_t)u * 32;
           if (v < hi) {
 #pragma unroll
             for (int p = 0; p < NR; ++p)
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const size_t v = base + (size_t)u * blockDim.x;
+          const size_t v = base + (size_t)u * 32;
           if (v < hi) {
             const uint4 r = fold_packet<T, A, OP, NR>(x[u]);
 #pragma unroll
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
       const int c = PUSH ? (rank + 1 + (int)(i / tpc)) % NR : (int)(i / tpc);
       size_t lo, hi;
       tile_range(c, i % tpc, lo, hi);
-      for (size_t v = lo + threadIdx.x; v < hi; v += blockDim.x) store_dst<T>(a, dst, v, alo, ld128(w + v * 16));
+      for (size_t v = lo + lane; v < hi; v += 32) store_dst<T>(a, dst, v, alo, ld128(w + v * 16));
     }
     phase_end(a, rank, 2);  // staging is read after barrier 1: hold peers until done
   }

@@ -240,16 +240,17 @@ int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, boo
   const size_t Vc = a.chunk;
   int blocks = (int)std::min<size_t>((Vc + (size_t)kThreads * 2 - 1) / ((size_t)kThreads * 2), (size_t)RP_MAX_BLOCKS);
   blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
-  // >= 4 tiles per block so the tail is short; 16..128 KiB tiles, whole warps' worth
-  size_t tv = Vc / ((size_t)blocks * 4);
-  tv = std::min<size_t>(std::max<size_t>(round_up(tv, 512), 1024), 8192);
+  // tiles are claimed per warp: >= 4 per warp so the tail is short, 4..64 KiB
+  const uint32_t warps = (uint32_t)blocks * (kThreads / 32);
+  size_t tv = Vc / ((size_t)warps * 4);
+  tv = std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
   a.tile_v = (uint32_t)tv;
   const uint32_t tpc = (uint32_t)((Vc + tv - 1) / tv);
   uint32_t claims[3] = {0, 0, 0};
-  if (push) claims[0] = tpc * (W - 1) + blocks;
-  else if (a.copy_in) claims[0] = tpc * W + blocks;
-  claims[1] = tpc + blocks;
-  if (a.copy_out) claims[2] = tpc * (push ? W - 1 : W) + blocks;
+  if (push) claims[0] = tpc * (W - 1) + warps;
+  else if (a.copy_in) claims[0] = tpc * W + warps;
+  claims[1] = tpc + warps;
+  if (a.copy_out) claims[2] = tpc * (push ? W - 1 : W) + warps;
   const bool used[3] = {true, true, a.copy_out != 0};
   for (int k = 0; k < 3; ++k) {
     a.tile_base[k] = c->tile_base[k];
