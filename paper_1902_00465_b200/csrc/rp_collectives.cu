@@ -324,7 +324,13 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   // Algorithm: deterministic in (bytes, world), hence identical on every rank.
   const size_t bytes = count * esz;
   if (algo == RP_ALGO_AUTO) {
-    const size_t oneshot_max = W <= 2 ? ((size_t)512 << 10) : (W <= 4 ? ((size_t)256 << 10) : ((size_t)128 << 10));
+    // crossover from tools/sweep.py: the push one-shot (multi-process, one barrier,
+    // ~8-12 us) beats the three-phase two-shot (~25-30 us floor) up to ~2 MiB at
+    // N=2 and the landing zone bounds it at RP_OS_REGION/N; virtual replicas use
+    // the pull forms, whose one-shot reads N times the message from HBM
+    size_t oneshot_max;
+    if (c->is_virtual) oneshot_max = W <= 2 ? ((size_t)512 << 10) : (W <= 4 ? ((size_t)256 << 10) : ((size_t)128 << 10));
+    else oneshot_max = std::min(RP_OS_REGION / (size_t)W, W <= 2 ? ((size_t)2 << 20) : ((size_t)1 << 20));
     algo = bytes <= oneshot_max ? RP_ALGO_ONESHOT : RP_ALGO_TWOSHOT;
   }
   if (algo != RP_ALGO_ONESHOT && algo != RP_ALGO_TWOSHOT)
