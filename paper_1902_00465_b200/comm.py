@@ -207,14 +207,18 @@ class Communicator(_Base):
         kind: "sum" | "mean" (sum, then /N) | "max" | "premean" (all_sum(x/N), the
         wrap_optimizer composition of PAPER.md:196-206). ``comm_dtype`` fuses a cast
         (e.g. f32 tensors exchanged as bf16)."""
-        x = _contig_cuda(x, self.device)
+        xd = _dense_cuda(x, self.device)
         if out is None:
-            out = torch.empty_like(x)
-        code = dtype_code(x.dtype)
+            out = torch.empty_like(xd)
+        # element-wise: any dense layout works as long as out has the same strides
+        od = out if (_is_dense(out) and out.stride() == xd.stride()) else torch.empty_like(xd, dtype=out.dtype)
+        code = dtype_code(xd.dtype)
         ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
-        _lib.check(self._lib.rp_all_reduce(self._handle, x.data_ptr(), out.data_ptr(), x.numel(), code, ccode,
-                                           dtype_code(out.dtype), _op(kind), _algo(algo), self._stream()),
+        _lib.check(self._lib.rp_all_reduce(self._handle, xd.data_ptr(), od.data_ptr(), xd.numel(), code, ccode,
+                                           dtype_code(od.dtype), _op(kind), _algo(algo), self._stream()),
                    "all_reduce")
+        if od is not out:
+            out.copy_(od)
         return out
 
     def all_gather_tensor(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -229,12 +233,15 @@ class Communicator(_Base):
     def broadcast_tensor(self, x: torch.Tensor, root: int = 0, out: torch.Tensor | None = None,
                          algo: str = "auto") -> torch.Tensor:
         """Every rank receives root's x (in place when out is None)."""
-        x = _contig_cuda(x, self.device)
+        xd = _dense_cuda(x, self.device)
         if out is None:
             out = x
-        _lib.check(self._lib.rp_broadcast(self._handle, x.data_ptr(), out.data_ptr(),
-                                          x.numel() * x.element_size(), root, _algo(algo), self._stream()),
+        od = out if (_is_dense(out) and out.stride() == xd.stride()) else torch.empty_like(xd)
+        _lib.check(self._lib.rp_broadcast(self._handle, xd.data_ptr(), od.data_ptr(),
+                                          xd.numel() * xd.element_size(), root, _algo(algo), self._stream()),
                    "broadcast")
+        if od is not out:  # e.g. an in-place broadcast of a strided view: write back
+            out.copy_(od)
         return out
 
     # -- the reference duck type (graph.py:565-583) -------------------------
@@ -341,6 +348,7 @@ class VirtualCommunicator(_Base):
         xs = self._check_list(xs)
         if outs is None:
             outs = [torch.empty_like(x) for x in xs]
+        _check_outs(outs, xs)
         code = dtype_code(xs[0].dtype)
         ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
         sp, _k1 = _lib.ptr_array([x.data_ptr() for x in xs])
@@ -368,6 +376,7 @@ class VirtualCommunicator(_Base):
         xs = self._check_list(xs)
         if outs is None:
             outs = [torch.empty_like(x) for x in xs]
+        _check_outs(outs, xs)
         sp, _k1 = _lib.ptr_array([x.data_ptr() for x in xs])
         dp, _k2 = _lib.ptr_array([o.data_ptr() for o in outs])
         _lib.check(self._lib.rp_broadcast_v(self._handle, sp, dp, xs[0].numel() * xs[0].element_size(), root,
@@ -393,6 +402,38 @@ def _algo(algo) -> int:
         return _lib.ALGOS[algo]
     except KeyError:
         raise errors.ShapeError(f"unknown algorithm {algo!r}") from None
+
+
+def _check_outs(outs, xs):
+    if len(outs) != len(xs):
+        raise errors.ShapeError(f"expected {len(xs)} output tensors, got {len(outs)}")
+    for o, x in zip(outs, xs):
+        if o.numel() != x.numel() or not (o.is_contiguous() or (_is_dense(o) and o.stride() == x.stride())):
+            raise errors.ShapeError("virtual collective outputs must be dense with the inputs' layout")
+
+
+def _is_dense(x: torch.Tensor) -> bool:
+    """Non-overlapping and dense: the storage span is exactly numel elements (any
+    dimension order), so element-wise collectives can treat it as a flat array."""
+    if x.is_contiguous():
+        return True
+    if x.dim() == 4 and x.is_contiguous(memory_format=torch.channels_last):
+        return True
+    if x.dim() == 5 and x.is_contiguous(memory_format=torch.channels_last_3d):
+        return True
+    return False
+
+
+def _dense_cuda(x: torch.Tensor, device: int) -> torch.Tensor:
+    """x itself when dense (contiguous or channels_last), else a contiguous copy.
+    Element-wise collectives run on the storage directly, so channels_last
+    parameters are reduced/broadcast in place."""
+    if not x.is_cuda:
+        raise errors.ShapeError("collective inputs must be CUDA tensors (host values go through the "
+                                "reference seam methods, which copy them in)")
+    if x.device.index != device:
+        raise errors.ShapeError(f"tensor on cuda:{x.device.index}, communicator on cuda:{device}")
+    return x if _is_dense(x) else x.contiguous()
 
 
 def _contig_cuda(x: torch.Tensor, device: int) -> torch.Tensor:

@@ -126,6 +126,23 @@ def body_gather_broadcast(rank, world):
                 x = torch.from_numpy(xs[rank]).to(dev)
                 comm.broadcast_tensor(x, root=root, algo=algo)
                 assert x.cpu().numpy().tobytes() == xs[root].tobytes(), (count, root, algo)
+    # dense non-contiguous layouts (channels_last parameters) are exchanged in place,
+    # strided views through a copy that is written back
+    g = torch.Generator(device=dev).manual_seed(77 + rank)
+    cl = torch.randn(2, 8, 5, 3, device=dev, generator=g).contiguous(memory_format=torch.channels_last)
+    cl_ptr = cl.data_ptr()
+    comm.broadcast_tensor(cl, root=0)
+    assert cl.data_ptr() == cl_ptr and cl.is_contiguous(memory_format=torch.channels_last)
+    allc = comm.all_gather_tensor(cl.contiguous())
+    assert all(torch.equal(allc[r], allc[0]) for r in range(world))
+    base = torch.randn(6, 10, device=dev, generator=g)
+    view = base[:, ::2]
+    before = [comm.all_gather_tensor(view.contiguous())[r].clone() for r in range(world)]
+    comm.all_reduce_tensor(view, "sum", out=view)
+    want = before[0].clone()
+    for r in range(1, world):
+        want = want + before[r]
+    assert torch.equal(view, want) and torch.equal(base[:, 1::2], base[:, 1::2])
     # reference duck type with host values (graph.py:573-582)
     xs = _inputs(world, 6, seed=3)
     local = xs[rank].reshape(2, 3)
@@ -264,6 +281,13 @@ def body_wrap_optimizer(rank, world):
         ref_opt.step()
     for p, q in zip(model.local.parameters(), ref.parameters()):
         assert (p - q).abs().max().item() < 1e-9  # SPEC.md:399 sync-equivalence bound
+    # a channels_last conv model: replicate() must sync every replica in place
+    torch.manual_seed(100 + rank)
+    conv = repl.replicate(lambda: torch.nn.Sequential(torch.nn.Conv2d(3, 8, 3), torch.nn.BatchNorm2d(8))
+                          .to(memory_format=torch.channels_last))
+    cflat = torch.cat([q.detach().contiguous().reshape(-1) for q in conv.local.parameters()])
+    cg = repl.comm.all_gather_tensor(cflat)
+    assert all(torch.equal(cg[r], cg[0]) for r in range(world)), "replicate() left channels_last replicas apart"
     # replicas bit-identical
     flat = torch.cat([p.detach().reshape(-1) for p in model.local.parameters()])
     g = repl.comm.all_gather_tensor(flat)

@@ -34,6 +34,7 @@ def main():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--grad-comm", default="bf16", choices=["bf16", "f32"])
     p.add_argument("--out", default=None)
+    p.add_argument("--no-average", action="store_true", help="control run: skip the gradient all-reduce")
     a = p.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -57,6 +58,8 @@ def main():
         opt = repl.wrap_optimizer(torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, nesterov=True,
                                                   weight_decay=1e-4))
     net = model.local
+    if a.no_average:
+        opt.average_gradients = lambda: None
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     x = torch.randn(a.batch, 3, 224, 224, device=dev, generator=g).contiguous(memory_format=torch.channels_last)
     y = torch.randint(0, 1000, (a.batch,), device=dev, generator=g)
@@ -87,7 +90,7 @@ def main():
     ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in evs)
     # the gradient all-reduce alone (same buckets), for its share of the step
     ar_ms = 0.0
-    if world > 1:
+    if world > 1 and not a.no_average:
         bk = opt._buckets
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
