@@ -35,6 +35,7 @@ def main():
     p.add_argument("--grad-comm", default="bf16", choices=["bf16", "f32"])
     p.add_argument("--out", default=None)
     p.add_argument("--no-average", action="store_true", help="control run: skip the gradient all-reduce")
+    p.add_argument("--diagnose", action="store_true", help="print per-phase GPU/host times of 8 steps")
     a = p.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -76,6 +77,32 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
+    if a.diagnose:  # per-phase GPU times (events) and host enqueue times of a few steps
+        import time as _t
+        rows = []
+        st = torch.cuda.current_stream(dev)
+        for _ in range(8):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            h = [_t.perf_counter()]
+            ev[0].record(st)
+            opt.zero_grad(set_to_none=False)
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                loss = lossf(net(x), y)
+            loss.backward()
+            ev[1].record(st)
+            h.append(_t.perf_counter())
+            opt.average_gradients()
+            ev[2].record(st)
+            h.append(_t.perf_counter())
+            opt.optimizer.step()
+            ev[3].record(st)
+            h.append(_t.perf_counter())
+            rows.append((ev, h))
+        torch.cuda.synchronize()
+        for ev, h in rows:
+            print(f"rank {rank} gpu fwdbwd {ev[0].elapsed_time(ev[1]):7.3f} avg {ev[1].elapsed_time(ev[2]):7.3f} "
+                  f"opt {ev[2].elapsed_time(ev[3]):7.3f} ms | host enqueue fwdbwd {1e3 * (h[1] - h[0]):7.3f} "
+                  f"avg {1e3 * (h[2] - h[1]):7.3f} opt {1e3 * (h[3] - h[2]):7.3f} ms", flush=True)
     if world > 1:
         torch.distributed.barrier()
     stream = torch.cuda.current_stream(dev)
