@@ -16,7 +16,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib, errors
-from .comm import Communicator, VirtualCommunicator, dtype_code
+from .comm import Communicator, VirtualCommunicator, _is_dense, dtype_code
 
 _ALIGN_ELEMS = 64  # keep every tensor's slot 128-byte aligned for 16-bit types
 
@@ -40,13 +40,20 @@ class _Bucket:
         self._offs_c = _lib.i64_array(self.offs)
 
     def _grads(self, r):
+        """The replica's gradients as dense storages. Pack/unpack copy storage order,
+        which is identical on every replica, so any dense layout (e.g. channels_last,
+        matching the parameter) is exchanged as is; a gradient is only re-laid out
+        (like its parameter, so the optimizer keeps its foreach fast path) when it
+        is not dense."""
         out = []
         for p in self.params[r]:
             if p.grad is None:
                 p.grad = torch.zeros_like(p)
             g = p.grad
-            if not g.is_contiguous():
-                p.grad = g = g.contiguous()
+            if not _is_dense(g):
+                d = torch.empty_like(p)
+                d.copy_(g)
+                p.grad = g = d
             out.append(g)
         return out
 
