@@ -537,9 +537,14 @@ class _CrossReplicaBNFn(torch.autograd.Function):
         sum_dy_xmu = torch.empty_like(sum_dy)
         loc_dy = torch.empty_like(sum_dy)
         loc_dy_xmu = torch.empty_like(sum_dy)
-        _lib.check(lib.rp_bn_bwd_stats(comm._handle, x.data_ptr(), dy.data_ptr(), code, rows, c, hw, layout,
-                                       mean.data_ptr(), sum_dy.data_ptr(), sum_dy_xmu.data_ptr(),
-                                       loc_dy.data_ptr(), loc_dy_xmu.data_ptr(), stream), "bn_bwd_stats")
+        args = [x, dy, mean, sum_dy, sum_dy_xmu, loc_dy, loc_dy_xmu]
+        if isinstance(comm, VirtualCommunicator):  # one local replica: per-replica pointer arrays
+            keep = [_lib.ptr_array([t.data_ptr()]) for t in args]
+            ptrs = [ctypes_cast(k[0]) for k in keep]
+        else:
+            ptrs = [t.data_ptr() for t in args]
+        _lib.check(lib.rp_bn_bwd_stats(comm._handle, ptrs[0], ptrs[1], code, rows, c, hw, layout, *ptrs[2:], stream),
+                   "bn_bwd_stats")
         dx = torch.empty_like(x)
         m_total = float(count.item()) if count is not None else float(rows * hw * comm.world)
         _lib.check(lib.rp_bn_bwd_apply(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), code, rows, c, hw, layout,
