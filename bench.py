@@ -211,7 +211,11 @@ def run_ours(args, rank, world, local):
     else:
         n = world
         comm = Communicator(device=local, pool_bytes=pool)
-        buf = comm.alloc(count, torch.float32)
+        if args.algo == "nvls":  # in-switch reduction: the buffer lives in the multicast region
+            comm.enable_nvls(args.bytes + (4 << 20))
+            buf = comm.alloc_nvls(count, torch.float32)
+        else:
+            buf = comm.alloc(count, torch.float32)
         buf.copy_(torch.randn(count, device=dev, generator=torch.Generator(device=dev).manual_seed(1234 + rank)))
 
         def step():

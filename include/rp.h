@@ -65,6 +65,8 @@ enum {
   RP_ALGO_TWOSHOT = 2, /* reduce-scatter (pull) + all-gather (push)           */
   RP_ALGO_DIRECT = 1,  /* broadcast: every rank pulls from root              */
   RP_ALGO_SCATTER = 2, /* broadcast: scatter from root + all-gather           */
+  RP_ALGO_NVLS = 3,    /* all_reduce in the NVSwitch (multimem), in place in the NVLS
+                          region; NOT rank-ordered: ~1e-6 relative (opt-in)    */
 };
 
 /* Status codes -> reference exception (errors.py). */
@@ -122,6 +124,22 @@ RP_API int rp_comm_check(rp_comm_t comm);
 
 /* Spin timeout for cross-rank waits, nanoseconds (default 20 s). */
 RP_API int rp_comm_set_timeout(rp_comm_t comm, uint64_t ns);
+
+/* ---- NVLS (NVLink SHARP) region ------------------------------------------ */
+/* A multicast object spanning all ranks' GPUs with `bytes` of each rank's memory
+ * bound to it (RP_ALGO_NVLS reduces inside the NVSwitch). Bootstrap order, every
+ * step on every rank unless noted:
+ *   rp_nvls_create (rank 0 creates + listens; returns a socket name in `name`)
+ *   [exchange `name`]  rp_nvls_serve (rank 0)  ||  rp_nvls_join(name) (others)
+ *   rp_nvls_add  [barrier]  rp_nvls_bind  [barrier]
+ * The handle travels as a POSIX fd over an abstract Unix socket (same host). */
+RP_API int rp_nvls_create(rp_comm_t comm, size_t bytes, char* name, size_t name_cap);
+RP_API int rp_nvls_serve(rp_comm_t comm);
+RP_API int rp_nvls_join(rp_comm_t comm, const char* name);
+RP_API int rp_nvls_add(rp_comm_t comm);
+RP_API int rp_nvls_bind(rp_comm_t comm);
+/* This rank's (unicast) view of the region: allocate fusion buckets here. */
+RP_API int rp_nvls_pool(rp_comm_t comm, void** base, size_t* bytes);
 
 /* ---- collectives (multi-process form: this rank's buffers) ---------------- */
 

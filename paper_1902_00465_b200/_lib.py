@@ -23,7 +23,8 @@ OPS = {"sum": SUM, "mean": MEAN, "max": MAX, "premean": PREMEAN}
 # algorithms
 AUTO, ONESHOT, TWOSHOT = 0, 1, 2
 DIRECT, SCATTER = 1, 2
-ALGOS = {"auto": AUTO, "oneshot": ONESHOT, "twoshot": TWOSHOT, "direct": DIRECT, "scatter": SCATTER}
+NVLS = 3
+ALGOS = {"auto": AUTO, "oneshot": ONESHOT, "twoshot": TWOSHOT, "direct": DIRECT, "scatter": SCATTER, "nvls": NVLS}
 # layouts
 NHWC, NCHW = 0, 1
 # status codes -> exception classes (errors.py)
@@ -74,6 +75,12 @@ SIGNATURES = {
                          _c_void_p, _c_void_p, _c_void_p]),
     "rp_bn_bwd_apply": (_i, [_c_void_p, _c_void_p, _c_void_p, _i, _i64, _i64, _i64, _i, _c_void_p,
                              _c_void_p, _c_void_p, _c_void_p, _c_void_p, _d, _c_void_p]),
+    "rp_nvls_create": (_i, [_c_void_p, _size_t, ctypes.c_char_p, _size_t]),
+    "rp_nvls_serve": (_i, [_c_void_p]),
+    "rp_nvls_join": (_i, [_c_void_p, ctypes.c_char_p]),
+    "rp_nvls_add": (_i, [_c_void_p]),
+    "rp_nvls_bind": (_i, [_c_void_p]),
+    "rp_nvls_pool": (_i, [_c_void_p, _pp, ctypes.POINTER(_size_t)]),
     "rp_pack": (_i, [_c_void_p, _i, _pp, _pi64, _pi64, _i, _i, _c_void_p]),
     "rp_unpack": (_i, [_c_void_p, _i, _pp, _pi64, _pi64, _i, _i, _c_void_p]),
 }

@@ -196,6 +196,46 @@ class Communicator(_Base):
         off = self._reserve(numel * esz)
         return tensor_at(self._pool_ptr(self.rank) + off, numel, dtype, self.device, self)
 
+    # -- NVLS (NVLink SHARP) region -------------------------------------------
+    def enable_nvls(self, nbytes: int, group=None) -> None:
+        """Bind ``nbytes`` of this rank's memory to one multicast object spanning all
+        ranks (include/rp.h rp_nvls_*). Collective over the group; the multicast fd
+        travels from rank 0 over a Unix socket, its name over torch.distributed."""
+        import torch.distributed as dist
+
+        if self.world < 2:
+            raise errors.ConfigurationError("NVLS needs at least two ranks")
+        name = ctypes.create_string_buffer(128)
+        _lib.check(self._lib.rp_nvls_create(self._handle, nbytes, name, 128), "nvls_create")
+        names = [None]
+        if self.rank == 0:
+            names = [name.value]
+        dist.broadcast_object_list(names, src=0, group=group)
+        if self.rank == 0:
+            _lib.check(self._lib.rp_nvls_serve(self._handle), "nvls_serve")
+        else:
+            _lib.check(self._lib.rp_nvls_join(self._handle, names[0]), "nvls_join")
+        _lib.check(self._lib.rp_nvls_add(self._handle), "nvls_add")
+        dist.barrier(group=group)
+        _lib.check(self._lib.rp_nvls_bind(self._handle), "nvls_bind")
+        dist.barrier(group=group)
+        base = ctypes.c_void_p()
+        size = ctypes.c_size_t()
+        _lib.check(self._lib.rp_nvls_pool(self._handle, ctypes.byref(base), ctypes.byref(size)), "nvls_pool")
+        self._nvls_base, self._nvls_size, self._nvls_used = base.value, size.value, 0
+
+    def alloc_nvls(self, numel: int, dtype: torch.dtype) -> torch.Tensor:
+        """Tensor inside the NVLS region (symmetric offsets); reduce it in place with
+        ``all_reduce_tensor(t, kind, out=t, algo="nvls")``."""
+        if not hasattr(self, "_nvls_base"):
+            raise errors.ConfigurationError("call enable_nvls() first")
+        esz = torch.empty((), dtype=dtype).element_size()
+        off = (self._nvls_used + _ALIGN - 1) // _ALIGN * _ALIGN
+        if off + numel * esz > self._nvls_size:
+            raise errors.ShapeError("NVLS region exhausted")
+        self._nvls_used = off + numel * esz
+        return tensor_at(self._nvls_base + off, numel, dtype, self.device, self)
+
     # -- torch-tensor collectives ------------------------------------------
     def _stream(self):
         return _stream_handle(self.device)

@@ -321,6 +321,12 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
     return RP_OK;
   }
 
+  if (algo == RP_ALGO_NVLS) {  // in-switch reduction, in place in the NVLS region
+    if (c->is_virtual) return rp_fail(RP_ERR_CONFIG, "all_reduce(nvls): needs a multi-process communicator");
+    if (src[0] != dst[0] || dtype_in != dtype_comm || dtype_out != dtype_comm)
+      return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): in place, without a cast");
+    return rp_nvls_launch(c, dst[0], count, dtype_comm, op, stream, dyn_launch, a);
+  }
   // Algorithm: deterministic in (bytes, world), hence identical on every rank.
   const size_t bytes = count * esz;
   if (algo == RP_ALGO_AUTO) {

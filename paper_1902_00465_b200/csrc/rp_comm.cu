@@ -346,6 +346,7 @@ int rp_comm_destroy(rp_comm_t c) {
   if (!c) return RP_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  rp_nvls_destroy(c);
   for (int r = 0; r < RP_MAX_RANKS; ++r) {
     if (!c->alloc[r]) continue;
     if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->alloc[r]);

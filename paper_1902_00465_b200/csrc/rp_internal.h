@@ -70,6 +70,7 @@ struct rp_comm {
   // source rank; identical on every rank) and cumulative tiles claimed per phase
   uint32_t ph_base[RP_PH_ROWS] = {};
   uint32_t tile_base[RP_PH_ROWS] = {};
+  void* nvls = nullptr;    // NvlsState (rp_nvls.cu): multicast-bound region, or NULL
   // end of the general staging window (see the layout above)
   size_t scratch_end() const { return pool_bytes - RP_BN_BYTES - 2 * RP_OS_REGION; }
   size_t oneshot_zone(int parity) const { return scratch_end() + (size_t)parity * RP_OS_REGION; }
@@ -148,3 +149,8 @@ int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, 
               cudaStream_t stream);
 // Blocks per rank for a collective kernel given its per-block occupancy.
 int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want);
+
+// NVLS (rp_nvls.cu)
+void rp_nvls_destroy(rp_comm* c);
+int rp_nvls_launch(rp_comm* c, const void* buf, size_t count, int dtype, int op, cudaStream_t stream,
+                   int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, bool, const char*), CollArgs& a);

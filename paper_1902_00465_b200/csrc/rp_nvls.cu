@@ -1,0 +1,374 @@
+// NVLS (NVLink SHARP) path: a multicast object spanning every rank's GPU, with
+// each rank's own memory bound to it. One `multimem.ld_reduce` returns the sum of
+// all N copies computed inside the NVSwitch, one `multimem.st` writes all N
+// copies. Per-GPU link traffic of an all-reduce drops from 2(N-1)/N*S per
+// direction (P2P two-shot) to about S -- the route past the P2P ceiling at N >= 4
+// (DESIGN.md §5, §8). The switch sums in its own order, so the result is NOT the
+// rank-ordered fold: this path is opt-in (RP_ALGO_NVLS) with a stated tolerance.
+//
+// Bootstrap: the multicast handle is a POSIX file descriptor (fabric handles are
+// not permitted on this pool, tools/mc_probe.cu), handed from rank 0 to its peers
+// over an abstract-namespace Unix socket with SCM_RIGHTS.
+#include <cuda.h>
+#include <string.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+
+#include "rp_allreduce.cuh"
+
+struct NvlsState {
+  CUmemGenericAllocationHandle mc = 0;
+  CUmemGenericAllocationHandle phys = 0;
+  CUdeviceptr mc_va = 0, uc_va = 0;
+  size_t size = 0, gran = 0;
+  int listen_fd = -1;
+  int share_fd = -1;
+  bool have_mc = false, added = false, bound = false;
+  size_t reserved = 0;
+};
+
+static NvlsState* nvls_of(rp_comm* c) { return (NvlsState*)c->nvls; }
+
+static int cu_fail(CUresult r, const char* what) {
+  const char* s = nullptr;
+  cuGetErrorString(r, &s);
+  return rp_fail(RP_ERR_CONFIG, std::string(what) + ": " + (s ? s : "CUDA driver error"));
+}
+#define CU_CHECK(x)                         \
+  do {                                      \
+    CUresult r_ = (x);                      \
+    if (r_ != CUDA_SUCCESS) return cu_fail(r_, #x); \
+  } while (0)
+
+static CUmulticastObjectProp mc_prop(rp_comm* c, size_t bytes) {
+  CUmulticastObjectProp p;
+  memset(&p, 0, sizeof(p));
+  p.numDevices = (unsigned)c->world;
+  p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  p.size = bytes;
+  return p;
+}
+
+static int nvls_size(rp_comm* c, size_t bytes, size_t* size, size_t* gran) {
+  CUmulticastObjectProp p = mc_prop(c, bytes);
+  size_t g = 0;
+  CU_CHECK(cuMulticastGetGranularity(&g, &p, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  *gran = g;
+  *size = (bytes + g - 1) / g * g;
+  return RP_OK;
+}
+
+static void abstract_addr(const char* name, sockaddr_un* a, socklen_t* len) {
+  memset(a, 0, sizeof(*a));
+  a->sun_family = AF_UNIX;
+  const size_t n = std::min(strlen(name), sizeof(a->sun_path) - 2);
+  memcpy(a->sun_path + 1, name, n);  // leading NUL: abstract namespace, no filesystem entry
+  *len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n);
+}
+
+extern "C" {
+
+int rp_nvls_create(rp_comm_t c, size_t bytes, char* name, size_t name_cap) {
+  if (!c || !name || name_cap < 64) return rp_fail(RP_ERR_INVALID, "rp_nvls_create: bad arguments");
+  if (c->is_virtual || c->world < 2) return rp_fail(RP_ERR_CONFIG, "NVLS needs a multi-process communicator");
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  RP_CUDA_CHECK(cudaFree(0));  // primary context current for the driver API
+  int mcs = 0;
+  CUdevice dev;
+  CU_CHECK(cuDeviceGet(&dev, c->device));
+  CU_CHECK(cuDeviceGetAttribute(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+  if (!mcs) return rp_fail(RP_ERR_CONFIG, "device does not support NVLS multicast");
+  if (!c->nvls) c->nvls = new NvlsState();
+  NvlsState* s = nvls_of(c);
+  int rc = nvls_size(c, bytes, &s->size, &s->gran);
+  if (rc) return rc;
+  name[0] = 0;
+  if (c->rank != 0) return RP_OK;
+  CUmulticastObjectProp p = mc_prop(c, s->size);
+  CU_CHECK(cuMulticastCreate(&s->mc, &p));
+  s->have_mc = true;
+  int fd = -1;
+  CU_CHECK(cuMemExportToShareableHandle(&fd, s->mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  s->share_fd = fd;
+  static std::atomic<int> counter{0};
+  snprintf(name, name_cap, "rp-nvls-%d-%d", (int)getpid(), counter++);
+  int ls = socket(AF_UNIX, SOCK_STREAM, 0);
+  if (ls < 0) return rp_fail(RP_ERR_CONFIG, "rp_nvls_create: socket() failed");
+  sockaddr_un a;
+  socklen_t len;
+  abstract_addr(name, &a, &len);
+  if (bind(ls, (sockaddr*)&a, len) != 0 || listen(ls, c->world) != 0) {
+    close(ls);
+    return rp_fail(RP_ERR_CONFIG, "rp_nvls_create: cannot bind/listen on the abstract socket");
+  }
+  s->listen_fd = ls;
+  return RP_OK;
+}
+
+// rank 0: hand the multicast fd to every peer (blocks until world-1 peers took it)
+int rp_nvls_serve(rp_comm_t c) {
+  if (!c || !c->nvls) return rp_fail(RP_ERR_INVALID, "rp_nvls_serve: call rp_nvls_create first");
+  NvlsState* s = nvls_of(c);
+  if (c->rank != 0) return RP_OK;
+  for (int i = 1; i < c->world; ++i) {
+    int conn = accept(s->listen_fd, nullptr, nullptr);
+    if (conn < 0) return rp_fail(RP_ERR_CONFIG, "rp_nvls_serve: accept() failed");
+    char byte = 'F';
+    iovec iov{&byte, 1};
+    char ctrl[CMSG_SPACE(sizeof(int))];
+    memset(ctrl, 0, sizeof(ctrl));
+    msghdr m;
+    memset(&m, 0, sizeof(m));
+    m.msg_iov = &iov;
+    m.msg_iovlen = 1;
+    m.msg_control = ctrl;
+    m.msg_controllen = sizeof(ctrl);
+    cmsghdr* cm = CMSG_FIRSTHDR(&m);
+    cm->cmsg_level = SOL_SOCKET;
+    cm->cmsg_type = SCM_RIGHTS;
+    cm->cmsg_len = CMSG_LEN(sizeof(int));
+    memcpy(CMSG_DATA(cm), &s->share_fd, sizeof(int));
+    const ssize_t n = sendmsg(conn, &m, 0);
+    close(conn);
+    if (n != 1) return rp_fail(RP_ERR_CONFIG, "rp_nvls_serve: sendmsg failed");
+  }
+  close(s->listen_fd);
+  s->listen_fd = -1;
+  return RP_OK;
+}
+
+// ranks != 0: receive the multicast fd from rank 0 and import the handle
+int rp_nvls_join(rp_comm_t c, const char* name) {
+  if (!c || !c->nvls || !name) return rp_fail(RP_ERR_INVALID, "rp_nvls_join: call rp_nvls_create first");
+  NvlsState* s = nvls_of(c);
+  if (c->rank == 0) return RP_OK;
+  int sock = socket(AF_UNIX, SOCK_STREAM, 0);
+  if (sock < 0) return rp_fail(RP_ERR_CONFIG, "rp_nvls_join: socket() failed");
+  sockaddr_un a;
+  socklen_t len;
+  abstract_addr(name, &a, &len);
+  int ok = -1;
+  for (int attempt = 0; attempt < 2000 && ok != 0; ++attempt) {  // rank 0 may not listen yet
+    ok = connect(sock, (sockaddr*)&a, len);
+    if (ok != 0) usleep(5000);
+  }
+  if (ok != 0) {
+    close(sock);
+    return rp_fail(RP_ERR_CONFIG, "rp_nvls_join: cannot reach rank 0's socket");
+  }
+  char byte = 0;
+  iovec iov{&byte, 1};
+  char ctrl[CMSG_SPACE(sizeof(int))];
+  msghdr m;
+  memset(&m, 0, sizeof(m));
+  m.msg_iov = &iov;
+  m.msg_iovlen = 1;
+  m.msg_control = ctrl;
+  m.msg_controllen = sizeof(ctrl);
+  const ssize_t n = recvmsg(sock, &m, 0);
+  close(sock);
+  cmsghdr* cm = CMSG_FIRSTHDR(&m);
+  if (n != 1 || !cm || cm->cmsg_type != SCM_RIGHTS) return rp_fail(RP_ERR_CONFIG, "rp_nvls_join: no fd received");
+  int fd;
+  memcpy(&fd, CMSG_DATA(cm), sizeof(int));
+  s->share_fd = fd;
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  CU_CHECK(cuMemImportFromShareableHandle(&s->mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+  s->have_mc = true;
+  return RP_OK;
+}
+
+// every rank: add its device (all ranks must finish this before anyone binds)
+int rp_nvls_add(rp_comm_t c) {
+  if (!c || !c->nvls || !nvls_of(c)->have_mc) return rp_fail(RP_ERR_INVALID, "rp_nvls_add: no multicast handle");
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  CUdevice dev;
+  CU_CHECK(cuDeviceGet(&dev, c->device));
+  CU_CHECK(cuMulticastAddDevice(nvls_of(c)->mc, dev));
+  nvls_of(c)->added = true;
+  return RP_OK;
+}
+
+// every rank: allocate its memory, bind it to the multicast object, map both views
+int rp_nvls_bind(rp_comm_t c) {
+  if (!c || !c->nvls || !nvls_of(c)->added) return rp_fail(RP_ERR_INVALID, "rp_nvls_bind: call rp_nvls_add first");
+  NvlsState* s = nvls_of(c);
+  RP_CUDA_CHECK(cudaSetDevice(c->device));
+  CUmemAllocationProp ap;
+  memset(&ap, 0, sizeof(ap));
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = c->device;
+  size_t pg = 0;
+  CU_CHECK(cuMemGetAllocationGranularity(&pg, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  const size_t g = std::max(pg, s->gran);
+  s->size = (s->size + g - 1) / g * g;
+  CU_CHECK(cuMemCreate(&s->phys, s->size, &ap, 0));
+  CU_CHECK(cuMulticastBindMem(s->mc, 0, s->phys, 0, s->size, 0));
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = c->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CU_CHECK(cuMemAddressReserve(&s->uc_va, s->size, g, 0, 0));
+  CU_CHECK(cuMemMap(s->uc_va, s->size, 0, s->phys, 0));
+  CU_CHECK(cuMemSetAccess(s->uc_va, s->size, &acc, 1));
+  CU_CHECK(cuMemAddressReserve(&s->mc_va, s->size, g, 0, 0));
+  CU_CHECK(cuMemMap(s->mc_va, s->size, 0, s->mc, 0));
+  CU_CHECK(cuMemSetAccess(s->mc_va, s->size, &acc, 1));
+  RP_CUDA_CHECK(cudaMemset((void*)s->uc_va, 0, s->size));
+  RP_CUDA_CHECK(cudaDeviceSynchronize());
+  s->bound = true;
+  return RP_OK;
+}
+
+int rp_nvls_pool(rp_comm_t c, void** base, size_t* bytes) {
+  if (!c || !base || !bytes) return rp_fail(RP_ERR_INVALID, "rp_nvls_pool: NULL argument");
+  if (!c->nvls || !nvls_of(c)->bound) return rp_fail(RP_ERR_CONFIG, "NVLS region not set up (rp_nvls_bind)");
+  *base = (void*)nvls_of(c)->uc_va;
+  *bytes = nvls_of(c)->size;
+  return RP_OK;
+}
+
+}  // extern "C"
+
+void rp_nvls_destroy(rp_comm* c) {
+  NvlsState* s = nvls_of(c);
+  if (!s) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (s->mc_va) {
+    cuMemUnmap(s->mc_va, s->size);
+    cuMemAddressFree(s->mc_va, s->size);
+  }
+  if (s->uc_va) {
+    cuMemUnmap(s->uc_va, s->size);
+    cuMemAddressFree(s->uc_va, s->size);
+  }
+  if (s->bound) {
+    CUdevice dev;
+    if (cuDeviceGet(&dev, c->device) == CUDA_SUCCESS) cuMulticastUnbind(s->mc, dev, 0, s->size);
+  }
+  if (s->phys) cuMemRelease(s->phys);
+  if (s->have_mc) cuMemRelease(s->mc);
+  if (s->listen_fd >= 0) close(s->listen_fd);
+  if (s->share_fd >= 0) close(s->share_fd);
+  delete s;
+  c->nvls = nullptr;
+}
+
+// ===========================================================================
+// K2n: NVLS all-reduce (in place in the multicast-bound region)
+//   barrier 0 (every rank's input is in place)
+//   tiles of chunk `rank` (per-warp claims): v = multimem.ld_reduce.add(mc + v)
+//     (the switch sums the N copies), scale for mean/premean, multimem.st(mc + v)
+//   barrier 1 (every rank's stores landed in every copy)
+// ===========================================================================
+namespace rp {
+
+template <int DT>
+__device__ __forceinline__ uint4 mc_ld_add(const void* p) {
+  uint4 r;
+  if constexpr (DT == RP_F32) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  } else if constexpr (DT == RP_BF16) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  } else {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  }
+  return r;
+}
+__device__ __forceinline__ void mc_st(void* p, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+template <int DT, int OP>
+__global__ void __launch_bounds__(kThreads) ar_nvls(const CollArgs a) {
+  using T = typename DType<DT>::T;
+  const int rank = a.rank;
+  char* mc = (char*)a.src[rank];  // the multicast view of this message
+  const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
+  const size_t Vc = a.chunk;
+  const uint32_t tv = a.tile_v;
+  const uint32_t tpc = (uint32_t)((Vc + tv - 1) / tv);
+  const int lane = threadIdx.x & 31;
+  rp_trace(a, 0);
+  if (!phase_end(a, rank, 0)) return;
+  const float inv = 1.0f / (float)a.world;
+  for (uint32_t j = claim_tile(a, rank, 1); j < tpc; j = claim_tile(a, rank, 1)) {
+    const size_t lo = (size_t)rank * Vc + (size_t)j * tv;
+    const size_t hi = std::min(std::min(lo + tv, (size_t)(rank + 1) * Vc), V);
+    constexpr int U = 4;
+    for (size_t base = lo + lane; base < hi; base += 32 * U) {
+      uint4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = base + (size_t)u * 32;
+        if (v < hi) r[u] = mc_ld_add<DT>(mc + v * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = base + (size_t)u * 32;
+        if (v >= hi) continue;
+        if (OP == RP_MEAN || OP == RP_PREMEAN) {
+          Pack16<T> p;
+          p.u = r[u];
+#pragma unroll
+          for (int e = 0; e < (int)(16 / sizeof(T)); ++e) p.e[e] = from_f32<T>(to_acc(p.e[e]) * inv);
+          r[u] = p.u;
+        }
+        mc_st(mc + v * 16, r[u]);
+      }
+    }
+  }
+  phase_end(a, rank, 1);
+  rp_trace(a, 7);
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+int rp_nvls_launch(rp_comm* c, const void* buf, size_t count, int dtype, int op, cudaStream_t stream,
+                   int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, bool, const char*), CollArgs& a) {
+  NvlsState* s = nvls_of(c);
+  if (!s || !s->bound) return rp_fail(RP_ERR_CONFIG, "all_reduce(nvls): NVLS region not set up");
+  const char* p = (const char*)buf;
+  const char* base = (const char*)s->uc_va;
+  const size_t esz = rp_dtype_size(dtype);
+  if (p < base || p + count * esz > base + s->size)
+    return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): buffer must live in the NVLS region (in place)");
+  if (dtype != RP_F32 && dtype != RP_BF16 && dtype != RP_F16)
+    return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): f32 / bf16 / f16 only");
+  if (op == RP_MAX) return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): sum / mean / premean only");
+  const size_t off = (size_t)(p - base);
+  if (off % 16) return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): buffer must be 16-byte aligned");
+  const size_t V = (count + (16 / esz) - 1) / (16 / esz);
+  if (off + V * 16 > s->size) return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): buffer tail exceeds the region");
+  a.count = count;
+  a.chunk = (V + c->world - 1) / c->world;
+  const void* fn = nullptr;
+#define RP_N(DT)                                                                       \
+  if (dtype == DT) {                                                                   \
+    if (op == RP_SUM) fn = (const void*)ar_nvls<DT, RP_SUM>;                            \
+    else if (op == RP_MEAN) fn = (const void*)ar_nvls<DT, RP_MEAN>;                     \
+    else fn = (const void*)ar_nvls<DT, RP_PREMEAN>;                                    \
+  }
+  RP_N(RP_F32)
+  RP_N(RP_BF16)
+  RP_N(RP_F16)
+#undef RP_N
+  a.src[c->rank] = (const void*)(s->mc_va + off);  // the kernel's multicast view
+  a.copy_in = a.copy_out = 0;
+  return dyn(c, fn, a, stream, false, "nvls");
+}

@@ -296,6 +296,37 @@ def body_wrap_optimizer(rank, world):
     repl.comm.close()
 
 
+def body_nvls(rank, world):
+    """In-switch all-reduce (multimem.ld_reduce / multimem.st). Not rank-ordered,
+    so checked against the f64 sum with a stated tolerance (north star: <=1e-6
+    relative, ordering-induced), plus bit-identical results on every rank."""
+    from paper_1902_00465_b200.comm import Communicator
+
+    comm = Communicator(device=rank, pool_bytes=32 << 20)
+    comm.enable_nvls(96 << 20)
+    for count in (4, 1000, 4099, 1 << 20, 12 << 20):
+        xs = _inputs(world, count, seed=500 + count)
+        buf = comm.alloc_nvls(count, torch.float32)
+        for kind in ("sum", "mean", "premean"):
+            buf.copy_(torch.from_numpy(xs[rank]))
+            comm.all_reduce_tensor(buf, kind, out=buf, algo="nvls")
+            got = buf.cpu().numpy().astype(np.float64)
+            want = np.sum(np.stack(xs).astype(np.float64), axis=0) / (1 if kind == "sum" else world)
+            err = np.linalg.norm(got - want) / np.linalg.norm(want)
+            assert err <= 1e-6, (count, kind, err)
+            g = comm.all_gather_tensor(buf)
+            assert all(torch.equal(g[r], g[0]) for r in range(world))
+        xb = [x.astype(np.float32) for x in _inputs(world, 50000, seed=9)]
+        bb = comm.alloc_nvls(50000, torch.bfloat16)
+        bb.copy_(torch.from_numpy(xb[rank]).to(torch.bfloat16))
+        comm.all_reduce_tensor(bb, "sum", out=bb, algo="nvls")
+        ref = sum(torch.from_numpy(x).to(torch.bfloat16).double() for x in xb)
+        rel = (bb.double().cpu() - ref).norm() / ref.norm()
+        assert rel < 4e-3, rel  # one bf16 rounding of an f32-accumulated sum
+    comm.check()
+    comm.close()
+
+
 def body_timeout(rank, world):
     """A rank that never joins makes the others time out (not hang) and report
     CollectiveAbortedError (SPEC.md:237 liveness; errors.py:68)."""
@@ -333,6 +364,10 @@ def test_cross_replica_bn_autograd_multiprocess():
 
 def test_wrap_optimizer_sync_equivalence_multiprocess():
     run_world("body_wrap_optimizer")
+
+
+def test_nvls_all_reduce_multiprocess():
+    run_world("body_nvls")
 
 
 def test_dead_rank_times_out():
