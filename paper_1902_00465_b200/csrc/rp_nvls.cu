@@ -19,7 +19,64 @@
 #include <atomic>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "rp_allreduce.cuh"
+
+// Driver-API entry points resolved at run time through the runtime
+// (cudaGetDriverEntryPoint): librp.so keeps no link-time dependency on
+// libcuda.so, so it still loads (and its C ABI can be inspected) on hosts
+// without a GPU driver.
+namespace {
+struct Driver {
+#define RP_DRV(name) PFN_##name name = nullptr;
+#define RP_DRV_ALL(X)                                                                             \
+  X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuGetErrorString) X(cuMemAddressFree) X(cuMemAddressReserve) \
+  X(cuMemCreate) X(cuMemExportToShareableHandle) X(cuMemGetAllocationGranularity)                 \
+  X(cuMemImportFromShareableHandle) X(cuMemMap) X(cuMemRelease) X(cuMemSetAccess) X(cuMemUnmap)   \
+  X(cuMulticastAddDevice) X(cuMulticastBindMem) X(cuMulticastCreate) X(cuMulticastGetGranularity) \
+  X(cuMulticastUnbind)
+  RP_DRV_ALL(RP_DRV)
+#undef RP_DRV
+  bool ok = false;
+};
+Driver g_drv;
+
+int load_driver() {
+  if (g_drv.ok) return RP_OK;
+#define RP_LOAD(name)                                                                            \
+  {                                                                                              \
+    void* fn = nullptr;                                                                          \
+    cudaDriverEntryPointQueryResult q;                                                           \
+    if (cudaGetDriverEntryPoint(#name, &fn, cudaEnableDefault, &q) != cudaSuccess || fn == nullptr) \
+      return rp_fail(RP_ERR_CONFIG, "CUDA driver entry point " #name " unavailable");           \
+    g_drv.name = (PFN_##name)fn;                                                                 \
+  }
+  RP_DRV_ALL(RP_LOAD)
+#undef RP_LOAD
+  g_drv.ok = true;
+  return RP_OK;
+}
+}  // namespace
+
+#define cuDeviceGet g_drv.cuDeviceGet
+#define cuDeviceGetAttribute g_drv.cuDeviceGetAttribute
+#define cuGetErrorString g_drv.cuGetErrorString
+#define cuMemAddressFree g_drv.cuMemAddressFree
+#define cuMemAddressReserve g_drv.cuMemAddressReserve
+#define cuMemCreate g_drv.cuMemCreate
+#define cuMemExportToShareableHandle g_drv.cuMemExportToShareableHandle
+#define cuMemGetAllocationGranularity g_drv.cuMemGetAllocationGranularity
+#define cuMemImportFromShareableHandle g_drv.cuMemImportFromShareableHandle
+#define cuMemMap g_drv.cuMemMap
+#define cuMemRelease g_drv.cuMemRelease
+#define cuMemSetAccess g_drv.cuMemSetAccess
+#define cuMemUnmap g_drv.cuMemUnmap
+#define cuMulticastAddDevice g_drv.cuMulticastAddDevice
+#define cuMulticastBindMem g_drv.cuMulticastBindMem
+#define cuMulticastCreate g_drv.cuMulticastCreate
+#define cuMulticastGetGranularity g_drv.cuMulticastGetGranularity
+#define cuMulticastUnbind g_drv.cuMulticastUnbind
 
 struct NvlsState {
   CUmemGenericAllocationHandle mc = 0;
@@ -78,6 +135,7 @@ int rp_nvls_create(rp_comm_t c, size_t bytes, char* name, size_t name_cap) {
   if (c->is_virtual || c->world < 2) return rp_fail(RP_ERR_CONFIG, "NVLS needs a multi-process communicator");
   RP_CUDA_CHECK(cudaSetDevice(c->device));
   RP_CUDA_CHECK(cudaFree(0));  // primary context current for the driver API
+  if (int rc0 = load_driver()) return rc0;
   int mcs = 0;
   CUdevice dev;
   CU_CHECK(cuDeviceGet(&dev, c->device));
@@ -204,6 +262,7 @@ int rp_nvls_bind(rp_comm_t c) {
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = c->device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // required to bind to the multicast object
   size_t pg = 0;
   CU_CHECK(cuMemGetAllocationGranularity(&pg, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
   const size_t g = std::max(pg, s->gran);
