@@ -212,7 +212,7 @@ def run_ours(args, rank, world, local):
         n = world
         comm = Communicator(device=local, pool_bytes=pool)
         if args.algo == "nvls":  # in-switch reduction: the buffer lives in the multicast region
-            comm.enable_nvls(args.bytes + (4 << 20))
+            comm.enable_nvls(2 * args.bytes + (4 << 20))  # timed buffer + the e2e buffer
             buf = comm.alloc_nvls(count, torch.float32)
         else:
             buf = comm.alloc(count, torch.float32)
@@ -306,7 +306,10 @@ def run_e2e(args, comm, world, n, count, dev, stream):
     reps = n if world == 1 else 1
     host_in = [torch.randn(count).pin_memory() for _ in range(reps)]
     host_out = torch.empty(count).pin_memory()
-    dev_in = [torch.empty(count, device=dev) for _ in range(reps)]
+    if args.algo == "nvls":  # the in-switch path reduces in place in the multicast region
+        dev_in = [comm.alloc_nvls(count, torch.float32)]
+    else:
+        dev_in = [torch.empty(count, device=dev) for _ in range(reps)]
 
     def step():
         for h, d in zip(host_in, dev_in):

@@ -302,7 +302,7 @@ def body_nvls(rank, world):
     relative, ordering-induced), plus bit-identical results on every rank."""
     from paper_1902_00465_b200.comm import Communicator
 
-    comm = Communicator(device=rank, pool_bytes=32 << 20)
+    comm = Communicator(device=rank, pool_bytes=128 << 20)
     comm.enable_nvls(96 << 20)
     for count in (4, 1000, 4099, 1 << 20, 12 << 20):
         xs = _inputs(world, count, seed=500 + count)
