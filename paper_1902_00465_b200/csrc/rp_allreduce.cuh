@@ -150,23 +150,44 @@ __device__ __forceinline__ void store_dst(const CollArgs& a, void* dst, size_t v
 // Claim the next tile of `phase` from this rank's local counter: one atomic per
 // WARP per tile, broadcast by shuffle -- no block-wide barrier in the main loop
 // (per-block claims cost two __syncthreads per tile: ~1/3 of the stall samples,
-// profiles/r01_ncu_ar_twoshot_dyn_n1.txt). Every warp ends with exactly one failing
-// claim, so a call advances the counter by ntiles + warps (host-tracked tile_base).
+// profiles/r01_ncu_ar_twoshot_dyn_n1.txt). The counters start every call at 0
+// (dyn_finish resets them), so nothing per call comes from the host.
 __device__ __forceinline__ uint32_t claim_tile(const CollArgs& a, int rank, int phase) {
   uint32_t t = 0;
-  if ((threadIdx.x & 31) == 0)
-    t = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + phase, 1u) - a.tile_base[phase];
+  if ((threadIdx.x & 31) == 0) t = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + phase, 1u);
   return __shfl_sync(0xffffffffu, t, 0);
+}
+
+// Per-call phase-barrier bases, read by every block at kernel start: rank p's
+// counter on phase row k must reach seen[k] + gridDim.x (all ranks run the same grid).
+struct PhaseBase {
+  uint32_t seen[3];
+};
+__device__ __forceinline__ PhaseBase phase_begin(const CollArgs& a, int rank) {
+  PhaseBase b;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) b.seen[k] = state_load(a.t, rank, RP_ST_PH_SEEN + k);
+  return b;
 }
 
 // Phase end for the dynamically scheduled kernels: count this block in, wait for
 // every block of every rank (trace slots 2p+1 / 2p+2).
-__device__ __forceinline__ bool phase_end(const CollArgs& a, int rank, int phase) {
+__device__ __forceinline__ bool phase_end(const CollArgs& a, int rank, int phase, const PhaseBase& pb) {
   phase_arrive(a.t, a.world, rank, phase);
   rp_trace(a, 2 * phase + 1);
-  const bool ok = phase_wait(a.t, a.world, a.timeout_ns, rank, phase, a.ph_target[phase]);
+  const bool ok = phase_wait(a.t, a.world, a.timeout_ns, rank, phase, pb.seen[phase] + gridDim.x);
   rp_trace(a, 2 * phase + 2);
   return ok;
+}
+
+// After the call's last phase barrier (every block of this rank has read the
+// bases and made its last claim): advance the bases of the phases used and zero
+// the tile counters for the next call. One thread of the rank's block 0.
+__device__ __forceinline__ void dyn_finish(const CollArgs& a, int rank, int phases, const PhaseBase& pb) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int k = 0; k < phases; ++k) state_store(a.t, rank, RP_ST_PH_SEEN + k, pb.seen[k] + gridDim.x);
+    for (int k = 0; k < 3; ++k) state_store(a.t, rank, RP_CTR_ROW * RP_MAX_RANKS + k, 0u);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -208,6 +229,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
     hi = std::min(std::min(lo + tv, (size_t)(c + 1) * Vc), V);
   };
   rp_trace(a, 0);
+  const PhaseBase pb = phase_begin(a, rank);
   const int lane = threadIdx.x & 31;
 
   // ---- phase 0 --------------------------------------------------------------
@@ -242,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
       for (size_t v = lo + lane; v < hi; v += 32) st128(mine + v * 16, load_src<T>(a, src, v, ali));
     }
   }
-  if (!phase_end(a, rank, 0)) return;
+  if (!phase_end(a, rank, 0, pb)) return;
 
   // ---- phase 1: fold my chunk, store the result on every rank ---------------
   {
@@ -284,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
       }
     }
   }
-  if (!phase_end(a, rank, 1)) return;
+  if (!phase_end(a, rank, 1, pb)) return;
 
   // ---- phase 2: results that landed in staging -> user dst ------------------
   if (a.copy_out) {
@@ -296,8 +318,9 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
       tile_range(c, i % tpc, lo, hi);
       for (size_t v = lo + lane; v < hi; v += 32) store_dst<T>(a, dst, v, alo, ld128(w + v * 16));
     }
-    phase_end(a, rank, 2);  // staging is read after barrier 1: hold peers until done
+    if (!phase_end(a, rank, 2, pb)) return;  // staging is read after barrier 1: hold peers until done
   }
+  dyn_finish(a, rank, a.copy_out ? 3 : 2, pb);
   rp_trace(a, 7);
 }
 
@@ -306,10 +329,11 @@ __global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
 //   rank r pushes its whole src into every peer's landing zone slot Z_p[r];
 //   barrier; every rank folds its own src and the N-1 received slots (local
 //   reads, ascending rank order) straight into its dst.
-// The landing zone alternates between two fixed regions by call parity
-// (a.read_off), so no trailing barrier is needed: a peer can only push into a
-// zone of the same parity after passing a barrier of the next call, i.e. after
-// we finished reading this one.
+// The landing zone alternates between two fixed regions by call parity (kept on
+// the device, zone_parity_begin), so no trailing barrier is needed: a peer can
+// only push into a zone of the same parity after passing a barrier of the next
+// call, whose kernel cannot start before this one completed everywhere.
+// a.read_off = parity-0 zone; parity 1 lies RP_OS_REGION above it.
 // ---------------------------------------------------------------------------
 template <int DT, int OP, int NR>
 __global__ void __launch_bounds__(kThreads) ar_oneshot_push(const CollArgs a) {
@@ -322,16 +346,20 @@ __global__ void __launch_bounds__(kThreads) ar_oneshot_push(const CollArgs a) {
   const size_t hi = std::min(lo + sub, V);
   const void* src = a.src[rank];
   const bool ali = aligned16(src);
+  const int es = RP_ST_BLK_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
+  const size_t zone = a.read_off + (size_t)zone_parity_begin(a.t, rank) * RP_OS_REGION;
   for (size_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
     const uint4 x = load_src<T>(a, src, v, ali);
 #pragma unroll
     for (int i = 1; i < NR; ++i) {
       const int p = (rank + i) % NR;
-      st128(a.t.data[p] + a.read_off + ((size_t)rank * V + v) * 16, x);
+      st128(a.t.data[p] + zone + ((size_t)rank * V + v) * 16, x);
     }
   }
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
-  const char* z = a.t.data[rank] + a.read_off;
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 1)) return;
+  epoch_end(a.t, rank, es, e0 + 1);
+  const char* z = a.t.data[rank] + zone;
   void* dst = a.dst[rank];
   const bool alo = aligned16(dst);
   for (size_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
@@ -355,9 +383,11 @@ __global__ void __launch_bounds__(kThreads) ar_oneshot(const CollArgs a) {
   const size_t sub = (V + gridDim.x - 1) / gridDim.x;
   const size_t lo = (size_t)blockIdx.x * sub;
   const size_t hi = std::min(lo + sub, V);
+  const int es = RP_ST_BLK_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
 
   if (a.copy_in && lo < hi) stage_in<T>(a, rank, a.t.data[rank] + a.read_off, lo, hi);
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 1)) return;
 
   const char* in[NR];
 #pragma unroll
@@ -394,7 +424,8 @@ __global__ void __launch_bounds__(kThreads) ar_oneshot(const CollArgs a) {
       }
     }
   }
-  rank_barrier(a, rank, blockIdx.x, a.epoch + 2);  // peers done reading our input
+  rank_barrier(a, rank, blockIdx.x, e0, 2);  // peers done reading our input
+  epoch_end(a.t, rank, es, e0 + 2);
 }
 
 // ---------------------------------------------------------------------------

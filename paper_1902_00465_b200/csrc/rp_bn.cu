@@ -50,7 +50,6 @@ struct ExArgs {
   int rank;  // -1: virtual (rank = blockIdx.y)
   int bwd;
   float eps;
-  uint32_t epoch;
   uint64_t timeout_ns;
 };
 
@@ -331,7 +330,9 @@ __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
     rec[1] = s2;
     rec[2] = a.local_count[rep];
   }
-  if (!rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, a.epoch + 1)) return;
+  const int es = RP_ST_BN_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
+  if (!rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, e0 + 1)) return;
   if (lane == 0 && c < C) {
     double A1 = 0.0, A2 = 0.0, Mt = 0.0;
     for (int p = 0; p < a.world; ++p) {  // ascending rank order
@@ -353,7 +354,8 @@ __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
     }
     if (c == 0 && a.count[rep]) *a.count[rep] = Mt;
   }
-  rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, a.epoch + 2);
+  rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, e0 + 2);
+  epoch_end(a.t, rank, es, e0 + 2);
 }
 
 // --- elementwise apply ----------------------------------------------------------
@@ -586,8 +588,6 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   e.cpb = cpb;
   const int blocks = (int)((ch + cpb - 1) / cpb);
   if (blocks > max_blocks) return rp_fail(RP_ERR_INVALID, "bn: too many channels for the exchange");
-  e.epoch = c->epoch;
-  c->epoch += 2;
   void* args[] = {&e};
   return rp_launch(c, (const void*)bn_exchange, dim3(blocks, c->is_virtual ? W : 1), dim3(kExThreads), args, 0,
                    stream);

@@ -80,9 +80,11 @@ __global__ void __launch_bounds__(kThreads) allgather_kernel(const CollArgs a, s
   const size_t B = a.count;
   const size_t lo = (size_t)blockIdx.x * a.chunk;
   const size_t hi = std::min(lo + a.chunk, B);
+  const int es = RP_ST_BLK_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
   if (a.copy_in && lo < hi)
     copy_bytes(a.t.data[rank] + a.read_off + rank * read_stride, (const char*)a.src[rank], lo, hi, vec);
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 1)) return;
   char* dst = (char*)a.dst[rank];
   if (lo < hi) {
     for (int i = 0; i < a.world; ++i) {
@@ -93,7 +95,8 @@ __global__ void __launch_bounds__(kThreads) allgather_kernel(const CollArgs a, s
       copy_bytes(d, src, lo, hi, vec);
     }
   }
-  rank_barrier(a, rank, blockIdx.x, a.epoch + 2);
+  rank_barrier(a, rank, blockIdx.x, e0, 2);
+  epoch_end(a.t, rank, es, e0 + 2);
 }
 
 // K4a: direct broadcast: every rank pulls root's pool copy.
@@ -102,13 +105,16 @@ __global__ void __launch_bounds__(kThreads) bcast_direct_kernel(const CollArgs a
   const size_t B = a.count;
   const size_t lo = (size_t)blockIdx.x * a.chunk;
   const size_t hi = std::min(lo + a.chunk, B);
+  const int es = RP_ST_BLK_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
   if (rank == a.root && a.copy_in && lo < hi)
     copy_bytes(a.t.data[rank] + a.read_off, (const char*)a.src[rank], lo, hi, vec);
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 1)) return;
   const char* src = a.t.data[a.root] + a.read_off;
   char* dst = (char*)a.dst[rank];
   if (lo < hi && dst != src) copy_bytes(dst, src, lo, hi, vec);
-  rank_barrier(a, rank, blockIdx.x, a.epoch + 2);
+  rank_barrier(a, rank, blockIdx.x, e0, 2);
+  epoch_end(a.t, rank, es, e0 + 2);
 }
 
 // K4b: scatter + all-gather broadcast. The message is cut into `world` chunks
@@ -120,20 +126,22 @@ __global__ void __launch_bounds__(kThreads) bcast_scatter_kernel(const CollArgs 
   const size_t s0 = (size_t)blockIdx.x * a.chunk;
   const size_t s1 = std::min(s0 + a.chunk, C);
   char* root_pool = a.t.data[a.root] + a.read_off;
+  const int es = RP_ST_BLK_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
   if (rank == a.root && a.copy_in && s0 < s1) {
     for (int c = 0; c < a.world; ++c) {
       const size_t lo = c * C + s0, hi = std::min(c * C + s1, B);
       if (lo < hi) copy_bytes(root_pool, (const char*)a.src[rank], lo, hi, vec);
     }
   }
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 1)) return;
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 1)) return;
   // scatter: pull my chunk from root into my pool staging (root keeps its own)
   char* my_stage = a.t.data[rank] + a.write_off;
   {
     const size_t lo = rank * C + s0, hi = std::min(rank * C + s1, B);
     if (lo < hi && rank != a.root) copy_bytes(my_stage, root_pool, lo, hi, vec);
   }
-  if (!rank_barrier(a, rank, blockIdx.x, a.epoch + 2)) return;
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 2)) return;
   // all-gather: pull chunk c from its owner's staging (root's chunks from root_pool)
   char* dst = (char*)a.dst[rank];
   for (int i = 0; i < a.world; ++i) {
@@ -144,7 +152,8 @@ __global__ void __launch_bounds__(kThreads) bcast_scatter_kernel(const CollArgs 
     if (dst + 0 == src) continue;
     copy_bytes(dst, src, lo, hi, vec);
   }
-  rank_barrier(a, rank, blockIdx.x, a.epoch + 3);
+  rank_barrier(a, rank, blockIdx.x, e0, 3);
+  epoch_end(a.t, rank, es, e0 + 3);
 }
 
 }  // namespace rp
@@ -232,10 +241,10 @@ int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t
 }
 
 // Launch a dynamically scheduled two-shot (ar_twoshot_dyn): pick the grid and the
-// tile size, hand the kernel its phase-barrier targets and tile-counter bases,
-// and advance the host's copies of those monotone counters (identical on every
-// rank because every quantity here is derived from (count, dtype, world, pool)).
-int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, bool push, const char* tag) {
+// tile size and launch. Everything per call that must agree across ranks (phase
+// barrier targets, tile counters) lives on the device (rp_internal.h RP_ST_*),
+// so the launch is the same every time and can be captured in a CUDA graph.
+int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, bool /*push*/, const char* tag) {
   const int W = c->world;
   const size_t Vc = a.chunk;
   int blocks = (int)std::min<size_t>((Vc + (size_t)kThreads * 2 - 1) / ((size_t)kThreads * 2), (size_t)RP_MAX_BLOCKS);
@@ -245,27 +254,7 @@ int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, boo
   size_t tv = Vc / ((size_t)warps * 4);
   tv = std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
   a.tile_v = (uint32_t)tv;
-  const uint32_t tpc = (uint32_t)((Vc + tv - 1) / tv);
-  uint32_t claims[3] = {0, 0, 0};
-  if (push) claims[0] = tpc * (W - 1) + warps;
-  else if (a.copy_in) claims[0] = tpc * W + warps;
-  claims[1] = tpc + warps;
-  if (a.copy_out) claims[2] = tpc * (push ? W - 1 : W) + warps;
-  const bool used[3] = {true, true, a.copy_out != 0};
-  for (int k = 0; k < 3; ++k) {
-    a.tile_base[k] = c->tile_base[k];
-    a.ph_target[k] = c->ph_base[k] + (uint32_t)blocks;
-  }
-  a.epoch = c->epoch;
-  c->calls += 1;
-  const int rc = launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream, tag);
-  if (rc == RP_OK) {
-    for (int k = 0; k < 3; ++k) {
-      c->tile_base[k] += claims[k];
-      if (used[k]) c->ph_base[k] += (uint32_t)blocks;
-    }
-  }
-  return rc;
+  return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream, tag);
 }
 
 void base_args(rp_comm* c, CollArgs& a) {
@@ -275,7 +264,6 @@ void base_args(rp_comm* c, CollArgs& a) {
   a.world = c->world;
   a.rank = c->is_virtual ? -1 : c->rank;
   a.timeout_ns = c->timeout_ns;
-  a.epoch = c->epoch;
 }
 
 }  // namespace
@@ -432,9 +420,6 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   const size_t per_block = (size_t)kThreads * 2;
   int blocks = (int)std::min<size_t>((V + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
   blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
-  a.epoch = c->epoch;
-  c->epoch += 2;
-  c->calls += 1;
   return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream, "oneshot_pull");
 }
 
@@ -449,14 +434,12 @@ static int launch_push(rp_comm* c, const void* const* src, void* const* dst, siz
   if (algo == RP_ALGO_ONESHOT && (size_t)W * V * 16 > RP_OS_REGION) algo = RP_ALGO_TWOSHOT;
   const size_t scratch = round_up(c->reserved, RP_ALIGN);
   const size_t scratch_end = c->scratch_end();
-  int epochs;
   size_t work;
   if (algo == RP_ALGO_ONESHOT) {
-    a.read_off = c->oneshot_zone((int)(c->calls & 1));
+    a.read_off = c->oneshot_zone(0);  // the kernel adds the device-side parity
     a.copy_out = 1;
     a.chunk = 0;
     work = V;
-    epochs = 1;
   } else {
     const size_t Vc = (V + W - 1) / W;
     const size_t qbytes = round_up((size_t)W * Vc * 16, RP_ALIGN);
@@ -502,9 +485,6 @@ static int launch_push(rp_comm* c, const void* const* src, void* const* dst, siz
   const size_t per_block = (size_t)kThreads * 2;
   int blocks = (int)std::min<size_t>((work + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
   blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
-  a.epoch = c->epoch;
-  c->epoch += epochs;
-  c->calls += 1;
   return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream,
                      algo == RP_ALGO_TWOSHOT ? "twoshot_push" : "oneshot_push");
 }
@@ -549,8 +529,6 @@ int rp_launch_all_gather(rp_comm* c, const void* const* src, void* const* dst, s
   const int blocks = rp_blocks_per_rank(c, (const void*)allgather_kernel, kThreads, std::max(want, 1));
   a.chunk = round_up((bytes + blocks - 1) / blocks, 16);
   int ivec = vec ? 1 : 0;
-  a.epoch = c->epoch;
-  c->epoch += 2;
   void* args[] = {&a, &read_stride, &ivec};
   return rp_launch(c, (const void*)allgather_kernel, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads),
                    args, 0, stream);
@@ -599,13 +577,11 @@ int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, si
     return rp_fail(RP_ERR_INVALID, "broadcast: message exceeds the staging pool");
   int ivec = vec ? 1 : 0;
   const size_t per_block_min = (size_t)16 * kThreads * 4;
-  a.epoch = c->epoch;
   if (algo == RP_ALGO_SCATTER) {
     const int want = (int)std::min<size_t>((bytes / W + per_block_min - 1) / per_block_min, (size_t)RP_MAX_BLOCKS);
     const int blocks = rp_blocks_per_rank(c, (const void*)bcast_scatter_kernel, kThreads, std::max(want, 1));
     size_t C = round_up((bytes + W - 1) / W, (size_t)16 * blocks);
     a.chunk = C / blocks;
-    c->epoch += 3;
     void* args[] = {&a, &C, &ivec};
     return rp_launch(c, (const void*)bcast_scatter_kernel, dim3(blocks, c->is_virtual ? W : 1),
                      dim3(kThreads), args, 0, stream);
@@ -614,7 +590,6 @@ int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, si
   const int want = (int)std::min<size_t>((bytes + per_block_min - 1) / per_block_min, (size_t)RP_MAX_BLOCKS);
   const int blocks = rp_blocks_per_rank(c, (const void*)bcast_direct_kernel, kThreads, std::max(want, 1));
   a.chunk = round_up((bytes + blocks - 1) / blocks, 16);
-  c->epoch += 2;
   void* args[] = {&a, &ivec};
   return rp_launch(c, (const void*)bcast_direct_kernel, dim3(blocks, c->is_virtual ? W : 1), dim3(kThreads),
                    args, 0, stream);

@@ -140,12 +140,50 @@ __device__ __forceinline__ void rp_trace(const CollArgs& a, int slot) {
   if (a.trace != nullptr && threadIdx.x == 0)
     a.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + slot] = globaltimer();
 }
-__device__ __forceinline__ bool rank_barrier(const CollArgs& a, int rank, int row, uint32_t value) {
-  const int k = (int)(value - a.epoch);
+// Barrier k (1..3) of this call for the current block: value e0 + k, where e0 is
+// the block's epoch read at kernel start (epoch_begin).
+__device__ __forceinline__ bool rank_barrier(const CollArgs& a, int rank, int row, uint32_t e0, int k) {
   rp_trace(a, 2 * k - 1);
-  const bool ok = rank_barrier(a.t, a.world, a.timeout_ns, rank, row, value);
+  const bool ok = rank_barrier(a.t, a.world, a.timeout_ns, rank, row, e0 + (uint32_t)k);
   rp_trace(a, 2 * k);
   return ok;
+}
+
+// ---------------------------------------------------------------------------
+// device-side sequencing state (rp_internal.h RP_ST_*): local to each rank
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t state_load(const RankTable& t, int rank, int idx) {
+  return *((volatile const uint32_t*)(t.sig[rank] + idx));
+}
+__device__ __forceinline__ void state_store(const RankTable& t, int rank, int idx, uint32_t v) {
+  *((volatile uint32_t*)(t.sig[rank] + idx)) = v;
+}
+// Epoch of barrier row `row` for this block (collective rows or BN rows).
+__device__ __forceinline__ uint32_t epoch_begin(const RankTable& t, int rank, int state_idx) {
+  return state_load(t, rank, state_idx);
+}
+// Advance the block's epoch by the number of barriers the call used (thread 0,
+// after the block's last barrier; every rank advances identically).
+__device__ __forceinline__ void epoch_end(const RankTable& t, int rank, int state_idx, uint32_t v) {
+  if (threadIdx.x == 0) state_store(t, rank, state_idx, v);
+}
+// Call-wide one-shot landing-zone parity: every block reads it at start and
+// counts itself in; the last block of the call flips it (all reads precede the
+// flip) and resets the counter. The same for every block of a call, which the
+// zone-reuse argument needs (rp_allreduce.cuh K1p).
+__device__ __forceinline__ uint32_t zone_parity_begin(const RankTable& t, int rank) {
+  __shared__ uint32_t s_par;
+  if (threadIdx.x == 0) {
+    s_par = state_load(t, rank, RP_ST_ZONE_PAR) & 1u;
+    __threadfence();
+    const uint32_t n = atomicAdd(t.sig[rank] + RP_ST_ZONE_PAR + 1, 1u);
+    if (n == gridDim.x - 1) {  // last reader of this call
+      state_store(t, rank, RP_ST_ZONE_PAR + 1, 0u);
+      state_store(t, rank, RP_ST_ZONE_PAR, s_par ^ 1u);
+    }
+  }
+  __syncthreads();
+  return s_par;
 }
 
 // ---------------------------------------------------------------------------

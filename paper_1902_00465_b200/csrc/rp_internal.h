@@ -22,6 +22,19 @@
 #define RP_PH_ROWS 4
 #define RP_CTR_ROW (RP_PH_ROW0 + RP_PH_ROWS)
 #define RP_ABORT_WORD ((RP_CTR_ROW + 4) * RP_MAX_RANKS)  // u32 index
+// Device-side sequencing state, local to each rank (never written by peers), in
+// the last 16 KiB of the signal region. Kernels read it at start and advance it
+// at the end, so launches carry no per-call host state and a captured CUDA graph
+// replays correctly (every rank runs the same sequence, so the copies agree):
+//   blk_epoch[b]  barrier epoch of block index b (collective rows 0..1023)
+//   bn_epoch[b]   same for the BN exchange rows
+//   zone_par[b]   one-shot landing-zone parity of block b
+//   ph_seen[k]    arrivals already consumed per source rank on phase row k
+#define RP_STATE_WORD (12 * 1024)
+#define RP_ST_BLK_EPOCH (RP_STATE_WORD)
+#define RP_ST_BN_EPOCH (RP_ST_BLK_EPOCH + RP_MAX_BLOCKS)
+#define RP_ST_ZONE_PAR (RP_ST_BN_EPOCH + 256)
+#define RP_ST_PH_SEEN (RP_ST_ZONE_PAR + RP_MAX_BLOCKS)
 #define RP_SIGNAL_BYTES (64 * 1024)  // signal region ahead of the data
 #define RP_ALIGN 256
 // Pool layout (every rank identical):
@@ -58,18 +71,12 @@ struct rp_comm {
   char* alloc[RP_MAX_RANKS] = {};   // allocations owned by this process
   bool ipc_opened[RP_MAX_RANKS] = {};
   RankTable table{};
-  uint32_t epoch = 0;      // monotone barrier epoch (one increment per barrier use)
   uint64_t timeout_ns = 20ull * 1000ull * 1000ull * 1000ull;
   int num_sms = 148;
   int max_coresident = 0;
   // BN scratch: per-split f64 partials (device memory, all local replicas)
   double* bn_partials = nullptr;
   size_t bn_partials_bytes = 0;
-  uint32_t calls = 0;      // collective calls issued (one-shot landing-zone parity)
-  // dynamically scheduled kernels: cumulative blocks through each phase row (per
-  // source rank; identical on every rank) and cumulative tiles claimed per phase
-  uint32_t ph_base[RP_PH_ROWS] = {};
-  uint32_t tile_base[RP_PH_ROWS] = {};
   void* nvls = nullptr;    // NvlsState (rp_nvls.cu): multicast-bound region, or NULL
   // end of the general staging window (see the layout above)
   size_t scratch_end() const { return pool_bytes - RP_BN_BYTES - 2 * RP_OS_REGION; }
@@ -102,13 +109,9 @@ struct CollArgs {
   int copy_out;         // pool[write_off] -> dst inside the kernel
   int dtype_in, dtype_out;
   int root;
-  uint32_t epoch;       // barrier values epoch+1, epoch+2, ...
   uint64_t timeout_ns;
   unsigned long long* trace;  // RP_TRACE analysis: per-block %globaltimer stamps, or NULL
-  // dynamically scheduled kernels
-  uint32_t tile_v;            // vectors (16 B) per tile
-  uint32_t ph_target[3];      // phase_wait targets (host-tracked cumulative block counts)
-  uint32_t tile_base[3];      // tile-claim counter values at the start of this call
+  uint32_t tile_v;            // dynamically scheduled kernels: vectors (16 B) per tile
 };
 
 // error plumbing

@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(kThreads) ar_nvls(const CollArgs a) {
   const uint32_t tpc = (uint32_t)((Vc + tv - 1) / tv);
   const int lane = threadIdx.x & 31;
   rp_trace(a, 0);
-  if (!phase_end(a, rank, 0)) return;
+  const PhaseBase pb = phase_begin(a, rank);
+  if (!phase_end(a, rank, 0, pb)) return;
   const float inv = 1.0f / (float)a.world;
   for (uint32_t j = claim_tile(a, rank, 1); j < tpc; j = claim_tile(a, rank, 1)) {
     const size_t lo = (size_t)rank * Vc + (size_t)j * tv;
@@ -390,7 +391,8 @@ __global__ void __launch_bounds__(kThreads) ar_nvls(const CollArgs a) {
       }
     }
   }
-  phase_end(a, rank, 1);
+  if (!phase_end(a, rank, 1, pb)) return;
+  dyn_finish(a, rank, 2, pb);
   rp_trace(a, 7);
 }
 

@@ -327,6 +327,49 @@ def body_nvls(rank, world):
     comm.close()
 
 
+def body_graph(rank, world):
+    """Each rank captures the same sequence of collectives in a CUDA graph and
+    replays it; device-side sequencing keeps the ranks in step across replays."""
+    from oracle import collectives as O
+    from paper_1902_00465_b200.comm import Communicator
+
+    dev = torch.device(f"cuda:{rank}")
+    comm = Communicator(device=rank, pool_bytes=64 << 20)
+    small = torch.empty(5000, device=dev)
+    big = torch.empty(3 << 20, device=dev)
+    bucket = comm.alloc(1 << 20, torch.float32)
+    o_small, o_big = torch.empty_like(small), torch.empty_like(big)
+
+    def seq():
+        comm.all_reduce_tensor(small, "sum", out=o_small)           # one-shot push
+        comm.all_reduce_tensor(big, "premean", out=o_big)           # two-shot push (staged)
+        comm.all_reduce_tensor(bucket, "premean", out=bucket)       # two-shot pull (pool, in place)
+
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        seq()
+    torch.cuda.current_stream(dev).wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        seq()
+    for it in range(5):
+        xs_s = _inputs(world, 5000, seed=1000 + it)
+        xs_b = _inputs(world, 3 << 20, seed=2000 + it)
+        xs_k = _inputs(world, 1 << 20, seed=3000 + it)
+        small.copy_(torch.from_numpy(xs_s[rank]))
+        big.copy_(torch.from_numpy(xs_b[rank]))
+        bucket.copy_(torch.from_numpy(xs_k[rank]))
+        g.replay()
+        torch.cuda.synchronize()
+        assert o_small.cpu().numpy().tobytes() == O.fold_sum(xs_s).tobytes(), it
+        assert o_big.cpu().numpy().tobytes() == O.fold_premean(xs_b).tobytes(), it
+        assert bucket.cpu().numpy().tobytes() == O.fold_premean(xs_k).tobytes(), it
+    comm.check()
+    comm.close()
+
+
 def body_timeout(rank, world):
     """A rank that never joins makes the others time out (not hang) and report
     CollectiveAbortedError (SPEC.md:237 liveness; errors.py:68)."""
@@ -368,6 +411,10 @@ def test_wrap_optimizer_sync_equivalence_multiprocess():
 
 def test_nvls_all_reduce_multiprocess():
     run_world("body_nvls")
+
+
+def test_cuda_graph_replay_multiprocess():
+    run_world("body_graph")
 
 
 def test_dead_rank_times_out():

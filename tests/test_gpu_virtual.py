@@ -218,6 +218,57 @@ def test_broadcast_nonzero_root_and_odd_bytes():
     assert host(outs[2]).tobytes() == np.concatenate([np.arange(7, dtype=np.float32) + r for r in range(n)]).tobytes()
 
 
+# --- CUDA graph capture ------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_collectives_replay_in_cuda_graph(n, impl):
+    """All sequencing state (barrier epochs, landing-zone parity, tile counters,
+    phase bases) lives on the device, so a captured sequence of collectives can be
+    replayed: every replay must give the oracle's answer for the new inputs."""
+    comm = VirtualCommunicator(n, device=0, pool_bytes=64 << 20)
+    small = [torch.empty(3000, device=DEV) for _ in range(n)]
+    big = [torch.empty(700001, device=DEV) for _ in range(n)]
+    gat = [torch.empty(777, device=DEV) for _ in range(n)]
+    o_small = [torch.empty_like(t) for t in small]
+    o_big = [torch.empty_like(t) for t in big]
+    o_gat = [torch.empty(n, 777, device=DEV) for _ in range(n)]
+    o_bc = [torch.empty_like(t) for t in gat]
+
+    def seq():
+        comm.all_reduce(small, "sum", outs=o_small, algo="oneshot")
+        comm.all_reduce(big, "premean", outs=o_big, algo="twoshot")
+        comm.all_gather(gat, outs=o_gat)
+        comm.broadcast(gat, root=n - 1, outs=o_bc)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        seq()  # warm up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        seq()
+    rng = np.random.default_rng(123)
+    for it in range(4):
+        vals = [[rng.standard_normal(t.numel()).astype(np.float32) for t in lst] for lst in (small, big, gat)]
+        for lst, vs in zip((small, big, gat), vals):
+            for t, v in zip(lst, vs):
+                t.copy_(to_dev(v))
+        g.replay()
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert host(o_small[r]).tobytes() == O.fold_sum(vals[0]).tobytes(), it
+            assert host(o_big[r]).tobytes() == O.fold_premean(vals[1]).tobytes(), it
+            assert host(o_gat[r]).tobytes() == np.concatenate(vals[2]).tobytes(), it
+            assert host(o_bc[r]).tobytes() == vals[2][n - 1].tobytes(), it
+    comm.check()
+    # eager calls after replays stay in step with the device-side state
+    outs = comm.all_reduce(big, "sum", algo="twoshot")
+    assert host(outs[0]).tobytes() == O.fold_sum([host(b) for b in big]).tobytes()
+    comm.close()
+
+
 # --- pack / unpack (K6) ----------------------------------------------------------
 
 def test_pack_unpack_roundtrip_with_cast():
