@@ -42,6 +42,8 @@ def main():
     p.add_argument("--global-batch", type=int, default=256)
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--graph", action="store_true",
+                   help="capture the whole learner step (both optimizers and their all-reduces) in a CUDA graph")
     a = p.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -60,8 +62,8 @@ def main():
     with repl.context():
         actor = repl.replicate(lambda: mlp([obs, 256, 256, act], nn.Tanh()))
         critic = repl.replicate(lambda: mlp([obs + act, 256, 256, atoms]))
-        actor_opt = repl.wrap_optimizer(torch.optim.Adam(actor.parameters(), lr=1e-4))
-        critic_opt = repl.wrap_optimizer(torch.optim.Adam(critic.parameters(), lr=1e-4))
+        actor_opt = repl.wrap_optimizer(torch.optim.Adam(actor.parameters(), lr=1e-4, capturable=a.graph))
+        critic_opt = repl.wrap_optimizer(torch.optim.Adam(critic.parameters(), lr=1e-4, capturable=a.graph))
     support = torch.linspace(-150, 150, atoms, device=dev)
     g = torch.Generator(device=dev).manual_seed(10 + rank)
     s = torch.randn(B, obs, device=dev, generator=g)
@@ -83,8 +85,24 @@ def main():
         actor_opt.step()
         return critic_loss, actor_loss
 
+    run = step
+    if a.graph:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                step()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            losses = step()
+
+        def run():
+            graph.replay()
+            return losses
     for _ in range(a.warmup):
-        step()
+        run()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -92,7 +110,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(a.steps):
-        cl, al = step()
+        cl, al = run()
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
@@ -117,7 +135,7 @@ def main():
         print(json.dumps({"metric": "D4PG learner steps/s", "value": 1e3 / ms, "unit": "steps/s", "n_gpus": world,
                           "global_batch": a.global_batch, "per_gpu_batch": B, "ms_per_step": ms,
                           "allreduce_ms_per_step": ar_ms, "grad_bytes_per_step": gb,
-                          "critic_loss": float(cl.item()), "actor_loss": float(al.item()),
+                          "critic_loss": float(cl.item()), "actor_loss": float(al.item()), "cuda_graph": a.graph,
                           "config": {"actor": "64-256-256-8 tanh", "critic": "72-256-256-51 (distributional)",
                                      "optimizers": "2 x Adam, both wrap_optimizer'd", "data": "synthetic replay"}}),
               flush=True)
