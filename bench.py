@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--replicas", type=int, default=8, help="replicas emulated on one GPU when N=1")
     p.add_argument("--kind", default="premean")
     p.add_argument("--algo", default="auto")
+    p.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
+                   help="place the buffers in an NVSwitch multicast region (auto: at >= 4 GPUs, where the "
+                        "in-switch reduction beats the P2P two-shot; the library then picks it under --algo auto)")
     p.add_argument("--ar-impl", default=None, choices=["push", "pull"],
                    help="force the all-reduce data-movement form (default: push multi-process, pull virtual)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,7 +187,8 @@ def _config(args, world):
                          f"replica, {n} replicas" + (f" emulated on 1 B200 (cooperative launch)" if world == 1
                                                       else f" on {world} B200 (one per process, NVLink P2P)")),
             "msg_bytes_per_replica": args.bytes, "replicas": n, "dtype": "f32", "op": args.kind,
-            "algo": args.algo, "in_place_pool": True, "l2": "flushed between steps (256 MiB write)",
+            "algo": getattr(args, "chosen_algo", args.algo), "algo_requested": args.algo,
+            "in_place_pool": True, "l2": "flushed between steps (256 MiB write)",
             "parallelism": f"dp{n}"}
 
 
@@ -211,15 +215,21 @@ def run_ours(args, rank, world, local):
     else:
         n = world
         comm = Communicator(device=local, pool_bytes=pool)
-        if args.algo == "nvls":  # in-switch reduction: the buffer lives in the multicast region
-            comm.enable_nvls(2 * args.bytes + (4 << 20))  # timed buffer + the e2e buffer
-            buf = comm.alloc_nvls(count, torch.float32)
-        else:
-            buf = comm.alloc(count, torch.float32)
+        args.use_nvls = args.algo == "nvls" or args.nvls == "on" or (args.nvls == "auto" and world >= 4)
+        if args.use_nvls:
+            try:  # in-switch reduction: the buffers live in the multicast region
+                comm.enable_nvls(2 * args.bytes + (4 << 20))  # timed buffer + the e2e buffer
+            except Exception as e:  # no multicast support on this box: the P2P kernels
+                if args.algo == "nvls":
+                    raise
+                args.use_nvls, args.nvls_error = False, str(e).splitlines()[0][:200]
+        buf = comm.alloc_nvls(count, torch.float32) if args.use_nvls else comm.alloc(count, torch.float32)
         buf.copy_(torch.randn(count, device=dev, generator=torch.Generator(device=dev).manual_seed(1234 + rank)))
 
         def step():
             comm.all_reduce_tensor(buf, args.kind, out=buf, algo=args.algo)
+
+        args.chosen_algo = comm.algorithm_for(buf, args.kind, out=buf, algo=args.algo)
 
     align = None
     if world > 1:
@@ -269,11 +279,22 @@ def run_ours(args, rank, world, local):
                     "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
                     "algorithmic_bytes_per_launch": alg_bytes, "kernel": "ar_twoshot<f32,premean,8>"}
     else:
+        # busBW = 2(N-1)/N * S / t against the per-direction link peak (the nccl-tests
+        # convention); the bytes one GPU's links actually carry per direction are
+        # 2(N-1)/N * S for the P2P two-shot and (N+1)/N * S for NVLS (the switch
+        # reduces and multicasts), so NVLS can exceed the link rate in busBW terms
+        algo = args.chosen_algo
+        link_bytes = (n + 1) / n * args.bytes if algo == "nvls" else 2.0 * (n - 1) / n * args.bytes
+        kernel = {"nvls": f"ar_nvls<f32,premean>", "twoshot": f"ar_twoshot_dyn<f32,premean,{n},pull>",
+                  "oneshot": f"ar_oneshot_push<f32,premean,{n}>"}[algo]
         roofline = {"bound": "nvlink", "achieved": per_gpu_bus, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                     "frac": per_gpu_bus / NVLINK_PEER_GBS, "frac_of_nominal_900": per_gpu_bus / NVLINK_NOMINAL_GBS,
                     "traffic": None, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
                     "algorithmic_bytes_per_launch": 2.0 * (n - 1) / n * args.bytes,
-                    "kernel": f"ar_twoshot<f32,premean,{n}>"}
+                    "link_bytes_per_direction": link_bytes,
+                    "link_gbs_per_direction": link_bytes / (ms / 1e3) / 1e9, "kernel": kernel}
+        if getattr(args, "nvls_error", None):
+            roofline["nvls_unavailable"] = args.nvls_error
 
     # e2e: host pinned buffers -> device -> all_reduce -> host, through the public API
     e2e = run_e2e(args, comm, world, n, count, dev, stream)
@@ -306,7 +327,7 @@ def run_e2e(args, comm, world, n, count, dev, stream):
     reps = n if world == 1 else 1
     host_in = [torch.randn(count).pin_memory() for _ in range(reps)]
     host_out = torch.empty(count).pin_memory()
-    if args.algo == "nvls":  # the in-switch path reduces in place in the multicast region
+    if getattr(args, "use_nvls", False):  # the in-switch path reduces in place in the multicast region
         dev_in = [comm.alloc_nvls(count, torch.float32)]
     else:
         dev_in = [torch.empty(count, device=dev) for _ in range(reps)]
@@ -334,7 +355,9 @@ def run_e2e(args, comm, world, n, count, dev, stream):
     ms = max_over_ranks(a.elapsed_time(b) / k, world)
     return {"value": busbw(args.bytes, n, ms / 1e3) * world, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": reps * count * 4, "d2h_bytes_per_step": count * 4,
-            "path": "pinned host -> cudaMemcpyAsync -> rp_all_reduce(_v) (staged, non-pool buffers) -> host"}
+            "path": "pinned host -> cudaMemcpyAsync -> rp_all_reduce(_v) -> host (" +
+                    ("in place in the NVLS region" if getattr(args, "use_nvls", False) else
+                     "staged, non-pool buffers") + ")"}
 
 
 def main():

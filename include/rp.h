@@ -66,7 +66,9 @@ enum {
   RP_ALGO_DIRECT = 1,  /* broadcast: every rank pulls from root              */
   RP_ALGO_SCATTER = 2, /* broadcast: scatter from root + all-gather           */
   RP_ALGO_NVLS = 3,    /* all_reduce in the NVSwitch (multimem), in place in the NVLS
-                          region; NOT rank-ordered: ~1e-6 relative (opt-in)    */
+                          region; NOT rank-ordered: ~1e-6 relative. AUTO picks it
+                          for in-place f32/bf16/f16 sum/mean/premean of >= 512 KiB
+                          inside the NVLS region at world >= 4 (RP_NVLS=0: never) */
 };
 
 /* Status codes -> reference exception (errors.py). */
@@ -150,6 +152,11 @@ RP_API int rp_nvls_pool(rp_comm_t comm, void** base, size_t* bytes);
  * src == dst is allowed. */
 RP_API int rp_all_reduce(rp_comm_t comm, const void* src, void* dst, size_t count, int dtype_in,
                   int dtype_comm, int dtype_out, int op, int algo, void* stream);
+
+/* The algorithm rp_all_reduce would run for these arguments (RP_ALGO_ONESHOT,
+ * RP_ALGO_TWOSHOT or RP_ALGO_NVLS) in *chosen; nothing is launched. */
+RP_API int rp_all_reduce_algo(rp_comm_t comm, const void* src, const void* dst, size_t count, int dtype_in,
+                              int dtype_comm, int dtype_out, int op, int algo, int* chosen);
 
 /* dst[r*bytes_per_rank ...] = src of rank r (rank order, graph.py:575-579). */
 RP_API int rp_all_gather(rp_comm_t comm, const void* src, void* dst, size_t bytes_per_rank, void* stream);

@@ -8,7 +8,10 @@ optional f32->bf16 cast fused in), reduced in place zero-copy with the
 ``premean`` fold -- the same divide-then-sum, ascending-rank arithmetic
  -- and unpacked back into ``param.grad`` (one K6 launch).
 Bit-for-bit the result equals the reference's per-gradient ``all_sum(g/R)``:
-packing is a copy and the fold is elementwise.
+packing is a copy and the fold is elementwise. When the communicator has an NVLS
+region with room (Replicator(nvls_bytes=...)), buckets are placed there instead and
+reduced inside the NVSwitch at >= 4 ranks: faster, but summed in switch order
+(within the north-star's 1e-6 relative tolerance rather than bit-exact).
 """
 
 from __future__ import annotations
@@ -34,7 +37,11 @@ class _Bucket:
             o += (n + _ALIGN_ELEMS - 1) // _ALIGN_ELEMS * _ALIGN_ELEMS
         self.offs = offs
         self.numel = o
-        buf = comm.alloc(o, comm_dtype)
+        esz = torch.empty((), dtype=comm_dtype).element_size()
+        if isinstance(comm, Communicator) and comm.nvls_free >= o * esz + 256:
+            buf = comm.alloc_nvls(o, comm_dtype)  # reduced inside the NVSwitch (rp.h RP_ALGO_NVLS)
+        else:
+            buf = comm.alloc(o, comm_dtype)
         self.flat = buf if isinstance(buf, list) else [buf]
         self._counts_c = _lib.i64_array(self.counts)
         self._offs_c = _lib.i64_array(self.offs)

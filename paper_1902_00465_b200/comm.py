@@ -224,9 +224,17 @@ class Communicator(_Base):
         _lib.check(self._lib.rp_nvls_pool(self._handle, ctypes.byref(base), ctypes.byref(size)), "nvls_pool")
         self._nvls_base, self._nvls_size, self._nvls_used = base.value, size.value, 0
 
+    @property
+    def nvls_free(self) -> int:
+        """Bytes still unallocated in the NVLS region (0 without one)."""
+        if not hasattr(self, "_nvls_base"):
+            return 0
+        return max(0, self._nvls_size - (self._nvls_used + _ALIGN - 1) // _ALIGN * _ALIGN)
+
     def alloc_nvls(self, numel: int, dtype: torch.dtype) -> torch.Tensor:
-        """Tensor inside the NVLS region (symmetric offsets); reduce it in place with
-        ``all_reduce_tensor(t, kind, out=t, algo="nvls")``."""
+        """Tensor inside the NVLS region (symmetric offsets: allocate in the same order
+        on every rank). In-place ``all_reduce_tensor(t, kind, out=t)`` reduces it in
+        the switch (algo "auto" at >= 4 ranks and >= 512 KiB, or algo="nvls")."""
         if not hasattr(self, "_nvls_base"):
             raise errors.ConfigurationError("call enable_nvls() first")
         esz = torch.empty((), dtype=dtype).element_size()
@@ -260,6 +268,19 @@ class Communicator(_Base):
         if od is not out:
             out.copy_(od)
         return out
+
+    def algorithm_for(self, x: torch.Tensor, kind: str = "sum", out: torch.Tensor | None = None,
+                      comm_dtype: torch.dtype | None = None, algo: str = "auto") -> str:
+        """The kernel family all_reduce_tensor(x, kind, out, comm_dtype, algo) runs:
+        "oneshot", "twoshot" or "nvls" (include/rp.h rp_all_reduce_algo)."""
+        out = x if out is None else out
+        code = dtype_code(x.dtype)
+        ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
+        chosen = ctypes.c_int(0)
+        _lib.check(self._lib.rp_all_reduce_algo(self._handle, x.data_ptr(), out.data_ptr(), x.numel(), code, ccode,
+                                                dtype_code(out.dtype), _op(kind), _algo(algo), ctypes.byref(chosen)),
+                   "all_reduce_algo")
+        return {1: "oneshot", 2: "twoshot", 3: "nvls"}[chosen.value]
 
     def all_gather_tensor(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """out[r] = x of rank r; out has shape (world,) + x.shape."""

@@ -159,7 +159,7 @@ __device__ __forceinline__ uint32_t claim_tile(const CollArgs& a, int rank, int 
 }
 
 // Per-call phase-barrier bases, read by every block at kernel start: rank p's
-// counter on phase row k must reach seen[k] + gridDim.x (all ranks run the same grid).
+// counter on phase row k must reach seen[k] + 1 (one arrival per rank per call).
 struct PhaseBase {
   uint32_t seen[3];
 };
@@ -175,18 +175,22 @@ __device__ __forceinline__ PhaseBase phase_begin(const CollArgs& a, int rank) {
 __device__ __forceinline__ bool phase_end(const CollArgs& a, int rank, int phase, const PhaseBase& pb) {
   phase_arrive(a.t, a.world, rank, phase);
   rp_trace(a, 2 * phase + 1);
-  const bool ok = phase_wait(a.t, a.world, a.timeout_ns, rank, phase, pb.seen[phase] + gridDim.x);
+  const bool ok = phase_wait(a.t, a.world, a.timeout_ns, rank, phase, pb.seen[phase] + 1u);
   rp_trace(a, 2 * phase + 2);
   return ok;
 }
 
 // After the call's last phase barrier (every block of this rank has read the
-// bases and made its last claim): advance the bases of the phases used and zero
-// the tile counters for the next call. One thread of the rank's block 0.
+// bases, made its last claim and arrived everywhere): advance the bases of the
+// phases used and zero the tile and arrival counters for the next call. One
+// thread of the rank's block 0.
 __device__ __forceinline__ void dyn_finish(const CollArgs& a, int rank, int phases, const PhaseBase& pb) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    for (int k = 0; k < phases; ++k) state_store(a.t, rank, RP_ST_PH_SEEN + k, pb.seen[k] + gridDim.x);
-    for (int k = 0; k < 3; ++k) state_store(a.t, rank, RP_CTR_ROW * RP_MAX_RANKS + k, 0u);
+    for (int k = 0; k < phases; ++k) state_store(a.t, rank, RP_ST_PH_SEEN + k, pb.seen[k] + 1u);
+    for (int k = 0; k < 3; ++k) {
+      state_store(a.t, rank, RP_CTR_ROW * RP_MAX_RANKS + k, 0u);
+      state_store(a.t, rank, RP_CTR_ROW * RP_MAX_RANKS + 4 + k, 0u);
+    }
   }
 }
 

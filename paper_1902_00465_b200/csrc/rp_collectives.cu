@@ -209,7 +209,8 @@ void fill_ptrs(rp_comm* c, CollArgs& a, const void* const* src, void* const* dst
 // Launch a collective kernel; with RP_TRACE=<file> (analysis only) also collect
 // the per-block %globaltimer stamps (rp_device.cuh rp_trace) and append them as
 // one JSON line per launch. Tracing synchronises the stream.
-int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t stream, const char* tag) {
+int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t stream, const char* tag,
+                int threads = kThreads) {
   const char* path = getenv("RP_TRACE");
   const size_t n = (size_t)grid.x * grid.y * 8;
   unsigned long long* buf = nullptr;
@@ -220,7 +221,7 @@ int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t
     a.trace = buf;
   }
   void* args[] = {&a};
-  const int rc = rp_launch(c, fn, grid, dim3(kThreads), args, 0, stream);
+  const int rc = rp_launch(c, fn, grid, dim3(threads), args, 0, stream);
   if (path) {
     std::vector<unsigned long long> h(n);
     cudaStreamSynchronize(stream);
@@ -244,17 +245,21 @@ int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t
 // tile size and launch. Everything per call that must agree across ranks (phase
 // barrier targets, tile counters) lives on the device (rp_internal.h RP_ST_*),
 // so the launch is the same every time and can be captured in a CUDA graph.
-int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, bool /*push*/, const char* tag) {
+int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, const char* tag, int max_blocks,
+               int threads, uint32_t tile_v) {
   const int W = c->world;
   const size_t Vc = a.chunk;
-  int blocks = (int)std::min<size_t>((Vc + (size_t)kThreads * 2 - 1) / ((size_t)kThreads * 2), (size_t)RP_MAX_BLOCKS);
-  blocks = rp_blocks_per_rank(c, fn, kThreads, std::max(blocks, 1));
+  int blocks = (int)std::min<size_t>((Vc + (size_t)threads * 2 - 1) / ((size_t)threads * 2),
+                                     (size_t)(max_blocks > 0 ? max_blocks : RP_MAX_BLOCKS));
+  blocks = rp_blocks_per_rank(c, fn, threads, std::max(blocks, 1));
   // tiles are claimed per warp: >= 4 per warp so the tail is short, 4..64 KiB
-  const uint32_t warps = (uint32_t)blocks * (kThreads / 32);
-  size_t tv = Vc / ((size_t)warps * 4);
-  tv = std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
-  a.tile_v = (uint32_t)tv;
-  return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream, tag);
+  if (tile_v == 0) {
+    const uint32_t warps = (uint32_t)blocks * (threads / 32);
+    size_t tv = Vc / ((size_t)warps * 4);
+    tile_v = (uint32_t)std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
+  }
+  a.tile_v = tile_v;
+  return launch_coll(c, fn, dim3(blocks, c->is_virtual ? W : 1), a, stream, tag, threads);
 }
 
 void base_args(rp_comm* c, CollArgs& a) {
@@ -267,6 +272,34 @@ void base_args(rp_comm* c, CollArgs& a) {
 }
 
 }  // namespace
+
+// Algorithm choice: deterministic in (arguments, world, NVLS placement), hence
+// identical on every rank (NVLS buffers are allocated symmetrically).
+int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
+                       int dtype_comm, int dtype_out, int op, int algo) {
+  if (algo != RP_ALGO_AUTO) return algo;
+  const int W = c->world;
+  const size_t bytes = count * rp_dtype_size(dtype_comm);
+  // NVLS (in-switch reduce + multicast store) moves (N+1)/N of the message per
+  // link direction against 2(N-1)/N for the two-shot: it wins from N=4 on, above
+  // the one-shot regime (tools/sweep.py, profiles/r01_sweep_nvls_n4.txt: 22.6 vs
+  // 38 us at 2 MiB, 168 vs 201 us at 64 MiB). The caller opts in by placing the
+  // buffer in the NVLS region; RP_NVLS=0 disables the automatic choice.
+  const char* ne = getenv("RP_NVLS");
+  if (!c->is_virtual && W >= 4 && !(ne && ne[0] == '0') && src[0] == dst[0] && dtype_in == dtype_comm &&
+      dtype_out == dtype_comm && op != RP_MAX &&
+      (dtype_comm == RP_F32 || dtype_comm == RP_BF16 || dtype_comm == RP_F16) && bytes >= ((size_t)512 << 10) &&
+      rp_nvls_covers(c, dst[0], bytes))
+    return RP_ALGO_NVLS;
+  // crossover from tools/sweep.py: the push one-shot (multi-process, one barrier,
+  // ~8-12 us) beats the two-phase two-shot (~20-30 us floor) up to ~2 MiB at
+  // N=2 and the landing zone bounds it at RP_OS_REGION/N; virtual replicas use
+  // the pull forms, whose one-shot reads N times the message from HBM
+  size_t oneshot_max;
+  if (c->is_virtual) oneshot_max = W <= 2 ? ((size_t)512 << 10) : (W <= 4 ? ((size_t)256 << 10) : ((size_t)128 << 10));
+  else oneshot_max = std::min(RP_OS_REGION / (size_t)W, W <= 2 ? ((size_t)2 << 20) : ((size_t)1 << 20));
+  return bytes <= oneshot_max ? RP_ALGO_ONESHOT : RP_ALGO_TWOSHOT;
+}
 
 int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, size_t count,
                          int dtype_in, int dtype_comm, int dtype_out, int op, int algo,
@@ -309,23 +342,13 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
     return RP_OK;
   }
 
+  const size_t bytes = count * esz;
+  algo = rp_resolve_ar_algo(c, src, (const void* const*)dst, count, dtype_in, dtype_comm, dtype_out, op, algo);
   if (algo == RP_ALGO_NVLS) {  // in-switch reduction, in place in the NVLS region
     if (c->is_virtual) return rp_fail(RP_ERR_CONFIG, "all_reduce(nvls): needs a multi-process communicator");
     if (src[0] != dst[0] || dtype_in != dtype_comm || dtype_out != dtype_comm)
       return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): in place, without a cast");
     return rp_nvls_launch(c, dst[0], count, dtype_comm, op, stream, dyn_launch, a);
-  }
-  // Algorithm: deterministic in (bytes, world), hence identical on every rank.
-  const size_t bytes = count * esz;
-  if (algo == RP_ALGO_AUTO) {
-    // crossover from tools/sweep.py: the push one-shot (multi-process, one barrier,
-    // ~8-12 us) beats the three-phase two-shot (~25-30 us floor) up to ~2 MiB at
-    // N=2 and the landing zone bounds it at RP_OS_REGION/N; virtual replicas use
-    // the pull forms, whose one-shot reads N times the message from HBM
-    size_t oneshot_max;
-    if (c->is_virtual) oneshot_max = W <= 2 ? ((size_t)512 << 10) : (W <= 4 ? ((size_t)256 << 10) : ((size_t)128 << 10));
-    else oneshot_max = std::min(RP_OS_REGION / (size_t)W, W <= 2 ? ((size_t)2 << 20) : ((size_t)1 << 20));
-    algo = bytes <= oneshot_max ? RP_ALGO_ONESHOT : RP_ALGO_TWOSHOT;
   }
   if (algo != RP_ALGO_ONESHOT && algo != RP_ALGO_TWOSHOT)
     return rp_fail(RP_ERR_INVALID, "all_reduce: unknown algorithm");
@@ -415,7 +438,7 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
   if (algo == RP_ALGO_TWOSHOT) {
     a.chunk = (V + W - 1) / W;
-    return dyn_launch(c, fn, a, stream, false, "twoshot_pull");
+    return dyn_launch(c, fn, a, stream, "twoshot_pull", 0, kThreads, 0);
   }
   const size_t per_block = (size_t)kThreads * 2;
   int blocks = (int)std::min<size_t>((V + per_block - 1) / per_block, (size_t)RP_MAX_BLOCKS);
@@ -477,7 +500,7 @@ static int launch_push(rp_comm* c, const void* const* src, void* const* dst, siz
     a.count = count;
     const void* fn = pick_ar_any(dtype_comm, op, algo, W, 1);
     if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
-    return dyn_launch(c, fn, a, stream, true, "twoshot_push");
+    return dyn_launch(c, fn, a, stream, "twoshot_push", 0, kThreads, 0);
   }
   a.count = count;
   const void* fn = pick_ar_any(dtype_comm, op, algo, W, 1);

@@ -424,6 +424,17 @@ int rp_all_reduce(rp_comm_t c, const void* src, void* dst, size_t count, int dty
   return rp_launch_all_reduce(c, s, d, count, dtype_in, dtype_comm, dtype_out, op, algo, (cudaStream_t)stream);
 }
 
+int rp_all_reduce_algo(rp_comm_t c, const void* src, const void* dst, size_t count, int dtype_in, int dtype_comm,
+                       int dtype_out, int op, int algo, int* chosen) {
+  RP_REQUIRE_READY(c, "rp_all_reduce_algo");
+  if (!chosen) return rp_fail(RP_ERR_INVALID, "rp_all_reduce_algo: NULL argument");
+  if (!rp_dtype_valid(dtype_comm)) return rp_fail(RP_ERR_INVALID, "rp_all_reduce_algo: unknown dtype");
+  const void* s[RP_MAX_RANKS] = {src};
+  const void* d[RP_MAX_RANKS] = {dst};
+  *chosen = rp_resolve_ar_algo(c, s, d, count, dtype_in, dtype_comm, dtype_out, op, algo);
+  return RP_OK;
+}
+
 int rp_all_reduce_v(rp_comm_t c, const void* const* src, void* const* dst, size_t count, int dtype_in,
                     int dtype_comm, int dtype_out, int op, int algo, void* stream) {
   RP_REQUIRE_READY(c, "rp_all_reduce_v");

@@ -113,14 +113,33 @@ __device__ __forceinline__ bool rank_barrier(const RankTable& t, int world, uint
 }
 
 // Rank-level phase barrier for dynamically scheduled kernels (any block may have
-// touched any tile, so every block of every rank must be counted). Arrive: each
-// block adds 1 to counter [phase row][rank] on every rank (release). Wait: every
-// block spins until its own counters [phase row][p] reach `target` (cumulative
-// number of blocks rank p has sent through this phase row, tracked by the host).
+// touched any tile, so every block of every rank must be counted). Hierarchical:
+// each block counts itself in on a LOCAL arrival counter (RP_CTR_ROW word
+// 4 + phase, zeroed by dyn_finish) with a gpu-scope acq_rel atomic; the block
+// that completes the count has thereby acquired every block's writes, issues ONE
+// fence.acq_rel.sys (cumulative: it covers those writes) and then a relaxed
+// increment of counter [phase row][rank] on every rank -- a release pattern
+// with a single system fence (red.release.sys per peer costs one fence each,
+// ~1.5 us apiece, tools/barrier_probe). Wait: every block spins (locally) until its
+// counters [phase row][p] reach `target` = calls already seen + 1. One remote
+// atomic and one system-scope fence per rank instead of per block: with every
+// block of every rank hitting the same peer word, the flat form cost 5-8 us per
+// barrier at 148-296 blocks (RP_TRACE, profiles/r01_trace_nvls.txt).
 __device__ __forceinline__ void phase_arrive(const RankTable& t, int world, int rank, int phase) {
-  __syncthreads();  // the block's writes happen-before the release
-  if (threadIdx.x < (unsigned)world)
-    red_release_sys_add(t.sig[threadIdx.x] + (size_t)(RP_PH_ROW0 + phase) * RP_MAX_RANKS + rank, 1u);
+  __syncthreads();  // the block's writes happen-before thread 0's release
+  if (threadIdx.x == 0) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old)
+                 : "l"(t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + 4 + phase)
+                 : "memory");
+    if (old == gridDim.x - 1) {  // last block of this rank
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int p = 0; p < world; ++p)
+        asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(t.sig[p] + (size_t)(RP_PH_ROW0 + phase) * RP_MAX_RANKS + rank)
+                     : "memory");
+    }
+  }
 }
 __device__ __forceinline__ bool phase_wait(const RankTable& t, int world, uint64_t timeout_ns, int rank, int phase,
                                            uint32_t target) {

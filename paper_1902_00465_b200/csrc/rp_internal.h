@@ -155,5 +155,10 @@ int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want);
 
 // NVLS (rp_nvls.cu)
 void rp_nvls_destroy(rp_comm* c);
+// [p, p + bytes) lies in this rank's bound NVLS region, 16-byte aligned
+bool rp_nvls_covers(rp_comm* c, const void* p, size_t bytes);
+// Algorithm rp_all_reduce runs (AUTO resolved): RP_ALGO_ONESHOT / TWOSHOT / NVLS
+int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
+                       int dtype_comm, int dtype_out, int op, int algo);
 int rp_nvls_launch(rp_comm* c, const void* buf, size_t count, int dtype, int op, cudaStream_t stream,
-                   int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, bool, const char*), CollArgs& a);
+                   int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t), CollArgs& a);

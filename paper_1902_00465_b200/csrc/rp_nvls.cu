@@ -296,6 +296,14 @@ int rp_nvls_pool(rp_comm_t c, void** base, size_t* bytes) {
 
 }  // extern "C"
 
+bool rp_nvls_covers(rp_comm* c, const void* p, size_t bytes) {
+  NvlsState* s = nvls_of(c);
+  if (!s || !s->bound) return false;
+  const char* q = (const char*)p;
+  const char* base = (const char*)s->uc_va;
+  return q >= base && q + bytes <= base + s->size && (size_t)(q - base) % 16 == 0;
+}
+
 void rp_nvls_destroy(rp_comm* c) {
   NvlsState* s = nvls_of(c);
   if (!s) return;
@@ -351,45 +359,53 @@ __device__ __forceinline__ void mc_st(void* p, uint4 v) {
                : "memory");
 }
 
+// One block of kNvlsThreads per SM, kNvlsU 16-byte requests in flight per
+// thread (~75K x 16 B per GPU: deeper queues only congest the switch,
+// profiles/r01_nvls_probe.txt). A tile is exactly one request per lane and
+// unroll step, so a warp finishes a tile in one switch round trip (short tail),
+// and the next tile's claim is issued before the current tile's loads.
+constexpr int kNvlsThreads = 128;
+constexpr int kNvlsU = 4;
+
 template <int DT, int OP>
-__global__ void __launch_bounds__(kThreads) ar_nvls(const CollArgs a) {
+__global__ void __launch_bounds__(kNvlsThreads) ar_nvls(const CollArgs a) {
   using T = typename DType<DT>::T;
   const int rank = a.rank;
   char* mc = (char*)a.src[rank];  // the multicast view of this message
   const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
   const size_t Vc = a.chunk;
-  const uint32_t tv = a.tile_v;
+  constexpr uint32_t tv = 32 * kNvlsU;
   const uint32_t tpc = (uint32_t)((Vc + tv - 1) / tv);
   const int lane = threadIdx.x & 31;
+  const size_t c_hi = std::min((size_t)(rank + 1) * Vc, V);
   rp_trace(a, 0);
   const PhaseBase pb = phase_begin(a, rank);
   if (!phase_end(a, rank, 0, pb)) return;
   const float inv = 1.0f / (float)a.world;
-  for (uint32_t j = claim_tile(a, rank, 1); j < tpc; j = claim_tile(a, rank, 1)) {
-    const size_t lo = (size_t)rank * Vc + (size_t)j * tv;
-    const size_t hi = std::min(std::min(lo + tv, (size_t)(rank + 1) * Vc), V);
-    constexpr int U = 4;
-    for (size_t base = lo + lane; base < hi; base += 32 * U) {
-      uint4 r[U];
+  uint32_t j = claim_tile(a, rank, 1);
+  while (j < tpc) {
+    const uint32_t next = claim_tile(a, rank, 1);
+    const size_t lo = (size_t)rank * Vc + (size_t)j * tv + lane;
+    uint4 r[kNvlsU];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t v = base + (size_t)u * 32;
-        if (v < hi) r[u] = mc_ld_add<DT>(mc + v * 16);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t v = base + (size_t)u * 32;
-        if (v >= hi) continue;
-        if (OP == RP_MEAN || OP == RP_PREMEAN) {
-          Pack16<T> p;
-          p.u = r[u];
-#pragma unroll
-          for (int e = 0; e < (int)(16 / sizeof(T)); ++e) p.e[e] = from_f32<T>(to_acc(p.e[e]) * inv);
-          r[u] = p.u;
-        }
-        mc_st(mc + v * 16, r[u]);
-      }
+    for (int u = 0; u < kNvlsU; ++u) {
+      const size_t v = lo + (size_t)u * 32;
+      if (v < c_hi) r[u] = mc_ld_add<DT>(mc + v * 16);
     }
+#pragma unroll
+    for (int u = 0; u < kNvlsU; ++u) {
+      const size_t v = lo + (size_t)u * 32;
+      if (v >= c_hi) continue;
+      if (OP == RP_MEAN || OP == RP_PREMEAN) {
+        Pack16<T> p;
+        p.u = r[u];
+#pragma unroll
+        for (int e = 0; e < (int)(16 / sizeof(T)); ++e) p.e[e] = from_f32<T>(to_acc(p.e[e]) * inv);
+        r[u] = p.u;
+      }
+      mc_st(mc + v * 16, r[u]);
+    }
+    j = next;
   }
   if (!phase_end(a, rank, 1, pb)) return;
   dyn_finish(a, rank, 2, pb);
@@ -401,7 +417,7 @@ __global__ void __launch_bounds__(kThreads) ar_nvls(const CollArgs a) {
 using namespace rp;
 
 int rp_nvls_launch(rp_comm* c, const void* buf, size_t count, int dtype, int op, cudaStream_t stream,
-                   int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, bool, const char*), CollArgs& a) {
+                   int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t), CollArgs& a) {
   NvlsState* s = nvls_of(c);
   if (!s || !s->bound) return rp_fail(RP_ERR_CONFIG, "all_reduce(nvls): NVLS region not set up");
   const char* p = (const char*)buf;
@@ -431,5 +447,5 @@ int rp_nvls_launch(rp_comm* c, const void* buf, size_t count, int dtype, int op,
 #undef RP_N
   a.src[c->rank] = (const void*)(s->mc_va + off);  // the kernel's multicast view
   a.copy_in = a.copy_out = 0;
-  return dyn(c, fn, a, stream, false, "nvls");
+  return dyn(c, fn, a, stream, "nvls", c->num_sms, kNvlsThreads, 32 * kNvlsU);
 }

@@ -162,7 +162,12 @@ class Replicator:
 
     def __init__(self, num_replicas: int | None = None, *, group=None, device: int | None = None,
                  pool_bytes: int = DEFAULT_POOL_BYTES, timeout_s: float = 20.0,
-                 grad_comm_dtype: torch.dtype | None = None, bucket_bytes: int | None = None):
+                 grad_comm_dtype: torch.dtype | None = None, bucket_bytes: int | None = None,
+                 nvls_bytes: int = 0):
+        """``nvls_bytes`` > 0 (multi-process, >= 2 ranks): bind that much memory per
+        rank to an NVSwitch multicast region and place gradient fusion buckets in it
+        while it has room, so wrap_optimizer's reduction runs in the switch
+        (RP_ALGO_NVLS; not rank-ordered -- leave 0 for bit-exact reference parity)."""
         import torch.distributed as dist
 
         mp = dist.is_available() and dist.is_initialized()
@@ -172,6 +177,8 @@ class Replicator:
             self.comm = Communicator(group=group, device=device, pool_bytes=pool_bytes, timeout_s=timeout_s)
             self.kind = "multi_gpu" if self.comm.world > 1 else "non"
             self._rv = None
+            if nvls_bytes > 0 and self.comm.world > 1:
+                self.comm.enable_nvls(int(nvls_bytes), group=group)
         else:
             n = 1 if num_replicas is None else int(num_replicas)
             if n < 1 or n > 8:

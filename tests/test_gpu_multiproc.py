@@ -323,8 +323,67 @@ def body_nvls(rank, world):
         ref = sum(torch.from_numpy(x).to(torch.bfloat16).double() for x in xb)
         rel = (bb.double().cpu() - ref).norm() / ref.norm()
         assert rel < 4e-3, rel  # one bf16 rounding of an f32-accumulated sum
+    # automatic choice (rp_resolve_ar_algo): in-place >= 512 KiB buffers in the
+    # region reduce in the switch from 4 ranks on; anything else stays P2P
+    big = comm.alloc_nvls(1 << 20, torch.float32)
+    small = comm.alloc_nvls(1000, torch.float32)
+    pool_buf = comm.alloc(1 << 20, torch.float32)
+    assert comm.algorithm_for(big, "mean", out=big) == ("nvls" if world >= 4 else "twoshot")
+    assert comm.algorithm_for(small, "mean", out=small) == "oneshot"
+    assert comm.algorithm_for(pool_buf, "mean", out=pool_buf) == "twoshot"
+    assert comm.algorithm_for(big, "max", out=big) == "twoshot"  # the switch has no ordered max here
+    os.environ["RP_NVLS"] = "0"
+    assert comm.algorithm_for(big, "mean", out=big) == "twoshot"
+    del os.environ["RP_NVLS"]
+    xs = _inputs(world, 1 << 20, seed=77)
+    big.copy_(torch.from_numpy(xs[rank]))
+    comm.all_reduce_tensor(big, "premean", out=big)
+    want = np.sum(np.stack(xs).astype(np.float64), axis=0) / world
+    got = big.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-6
     comm.check()
     comm.close()
+
+
+def body_wrap_nvls(rank, world):
+    """wrap_optimizer with fusion buckets in the NVLS region (Replicator(nvls_bytes)):
+    the same training as the single-device oracle on the concatenated batch, within
+    the f32 ordering tolerance, and replicas stay bit-identical (the multicast store
+    writes one value to every rank)."""
+    from paper_1902_00465_b200.replicator import Replicator
+
+    dev = torch.device(f"cuda:{rank}")
+    repl = Replicator(device=rank, pool_bytes=32 << 20, nvls_bytes=16 << 20)
+    torch.manual_seed(rank)
+    with repl.context():
+        model = repl.replicate(lambda: torch.nn.Sequential(torch.nn.Linear(784, 256), torch.nn.ReLU(),
+                                                           torch.nn.Linear(256, 10)))
+        opt = repl.wrap_optimizer(torch.optim.SGD(model.parameters(), lr=0.1))
+    torch.manual_seed(0)
+    ref = torch.nn.Sequential(torch.nn.Linear(784, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).double().to(dev)
+    with torch.no_grad():
+        for p, q in zip(ref.parameters(), model.local.parameters()):
+            p.copy_(q.double())
+    ref_opt = torch.optim.SGD(ref.parameters(), lr=0.1)
+    B = 16
+    for step in range(3):
+        g = torch.Generator().manual_seed(step)
+        xs = torch.randn(world * B, 784, generator=g).to(dev)
+        ys = torch.randint(0, 10, (world * B,), generator=g).to(dev)
+        opt.zero_grad()
+        torch.nn.functional.cross_entropy(model(xs[rank * B:(rank + 1) * B]), ys[rank * B:(rank + 1) * B]).backward()
+        opt.step()
+        ref_opt.zero_grad()
+        torch.nn.functional.cross_entropy(ref(xs.double()), ys).backward()
+        ref_opt.step()
+    bk = opt._buckets.buckets[0]
+    assert repl.comm.algorithm_for(bk.flat[0], "premean", out=bk.flat[0]) == ("nvls" if world >= 4 else "twoshot")
+    for p, q in zip(model.local.parameters(), ref.parameters()):
+        assert (p.double() - q).abs().max().item() < 1e-5
+    flat = torch.cat([p.detach().reshape(-1) for p in model.local.parameters()])
+    gathered = repl.comm.all_gather_tensor(flat)
+    assert all(torch.equal(gathered[r], gathered[0]) for r in range(world))
+    repl.comm.close()
 
 
 def body_graph(rank, world):
@@ -411,6 +470,10 @@ def test_wrap_optimizer_sync_equivalence_multiprocess():
 
 def test_nvls_all_reduce_multiprocess():
     run_world("body_nvls")
+
+
+def test_wrap_optimizer_nvls_buckets_multiprocess():
+    run_world("body_wrap_nvls")
 
 
 def test_cuda_graph_replay_multiprocess():

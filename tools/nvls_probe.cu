@@ -1,73 +1,70 @@
-// NVLS microbenchmark (single process, all visible GPUs): multicast object bound
-// to every GPU; measures multimem.ld_reduce (in-switch sum) and multimem.st
-// bandwidth per GPU with different unroll depths and grids. Design evidence for
-// the RP_ALGO_NVLS kernel.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/nvls_probe tools/nvls_probe.cu -lcuda
+// NVLS microbenchmark (single process, all visible GPUs): a multicast object bound
+// to every GPU; times multimem.ld_reduce (in-switch sum), multimem.st, and the
+// fused ld_reduce -> st all-reduce body, each iteration after an L2 flush (as in
+// bench.py), as max over GPUs. Sweeps unroll, grid, block size and memory
+// semantics (weak vs .relaxed.sys). Design evidence for the RP_ALGO_NVLS kernel.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/nvls_probe tools/nvls_probe.cu -lcuda
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <algorithm>
 #include <vector>
 #define CK(x) do { CUresult r = (x); if (r != CUDA_SUCCESS) { const char* s; cuGetErrorString(r, &s); printf("%s:%d %s -> %s\n", __FILE__, __LINE__, #x, s); exit(1);} } while (0)
 #define RK(x) do { cudaError_t r = (x); if (r != cudaSuccess) { printf("%s:%d %s -> %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(r)); exit(1);} } while (0)
 
-template <int U>
-__global__ void k_ldred(char* mc, size_t lo, size_t hi, float4* sink) {
+template <bool WEAK>
+__device__ __forceinline__ float4 ldr(const char* p) {
+  float4 r;
+  if (WEAK)
+    asm volatile("multimem.ld_reduce.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p) : "memory");
+  else
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p) : "memory");
+  return r;
+}
+template <bool WEAK>
+__device__ __forceinline__ void mst(char* p, float4 v) {
+  if (WEAK)
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+  else
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w) : "memory");
+}
+
+// MODE 0: ld_reduce only, 1: st only, 2: ld_reduce -> st (the all-reduce body)
+template <int MODE, int U, bool WEAK>
+__global__ void k_body(char* mc, size_t lo, size_t hi, float4* sink) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x * 16;
   float acc = 0.f;
-  for (size_t base = lo + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; base < hi;
-       base += (size_t)gridDim.x * blockDim.x * 16 * U) {
+  for (size_t base = lo + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; base < hi; base += stride * U) {
     float4 r[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      size_t o = base + (size_t)u * gridDim.x * blockDim.x * 16;
-      if (o < hi)
-        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(r[u].x), "=f"(r[u].y), "=f"(r[u].z), "=f"(r[u].w) : "l"(mc + o) : "memory");
-      else r[u] = make_float4(0, 0, 0, 0);
+      const size_t o = base + (size_t)u * stride;
+      r[u] = make_float4(1.f, 2.f, 3.f, 4.f);
+      if (MODE != 1 && o < hi) r[u] = ldr<WEAK>(mc + o);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) acc += r[u].x + r[u].y + r[u].z + r[u].w;
+    for (int u = 0; u < U; ++u) {
+      const size_t o = base + (size_t)u * stride;
+      if (MODE == 0) acc += r[u].x + r[u].y + r[u].z + r[u].w;
+      else if (o < hi) mst<WEAK>(mc + o, r[u]);
+    }
   }
   if (acc == 12345.f) sink[0] = make_float4(acc, 0, 0, 0);
 }
-template <int U>
-__global__ void k_st(char* mc, size_t lo, size_t hi) {
-  for (size_t base = lo + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; base < hi;
-       base += (size_t)gridDim.x * blockDim.x * 16 * U) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      size_t o = base + (size_t)u * gridDim.x * blockDim.x * 16;
-      if (o < hi)
-        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + o), "f"(1.f), "f"(2.f),
-                     "f"(3.f), "f"(4.f) : "memory");
-    }
-  }
-}
-template <int U>
-__global__ void k_both(char* mc, size_t lo, size_t hi) {
-  for (size_t base = lo + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; base < hi;
-       base += (size_t)gridDim.x * blockDim.x * 16 * U) {
-    float4 r[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      size_t o = base + (size_t)u * gridDim.x * blockDim.x * 16;
-      if (o < hi)
-        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(r[u].x), "=f"(r[u].y), "=f"(r[u].z), "=f"(r[u].w) : "l"(mc + o) : "memory");
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      size_t o = base + (size_t)u * gridDim.x * blockDim.x * 16;
-      if (o < hi)
-        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + o), "f"(r[u].x),
-                     "f"(r[u].y), "f"(r[u].z), "f"(r[u].w) : "memory");
-    }
-  }
+
+__global__ void k_flush(float4* p, size_t n, float v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_float4(v, v, v, v);
 }
 
 int main(int argc, char** argv) {
-  size_t bytes = (size_t)(argc > 1 ? atoi(argv[1]) : 256) << 20;
+  size_t bytes = (size_t)(argc > 1 ? atoi(argv[1]) : 64) << 20;
   CK(cuInit(0));
   int n = 0;
   RK(cudaGetDeviceCount(&n));
@@ -104,41 +101,61 @@ int main(int argc, char** argv) {
     CK(cuMemMap(mcva[d], bytes, 0, mc, 0));
     CK(cuMemSetAccess(mcva[d], bytes, &acc, 1));
   }
+  const size_t flush_n = (256u << 20) / 16;
   float4* sink[8];
+  float4* fl[8];
   cudaStream_t st[8];
-  for (int d = 0; d < n; ++d) { RK(cudaSetDevice(d)); RK(cudaMalloc(&sink[d], 64)); RK(cudaStreamCreate(&st[d])); }
-  printf("%d GPUs, %zu MiB, per-GPU chunk %zu MiB (GB/s per GPU of chunk bytes)\n", n, bytes >> 20, (bytes / n) >> 20);
-  auto run = [&](const char* name, auto launch) {
-    for (int w = 0; w < 2; ++w)
-      for (int d = 0; d < n; ++d) { RK(cudaSetDevice(d)); launch(d); }
-    for (int d = 0; d < n; ++d) { RK(cudaSetDevice(d)); RK(cudaDeviceSynchronize()); }
-    cudaEvent_t e0[8], e1[8];
-    const int it = 5;
-    for (int d = 0; d < n; ++d) {
-      RK(cudaSetDevice(d)); RK(cudaEventCreate(&e0[d])); RK(cudaEventCreate(&e1[d]));
-      RK(cudaEventRecord(e0[d], st[d]));
-      for (int i = 0; i < it; ++i) launch(d);
-      RK(cudaEventRecord(e1[d], st[d]));
-    }
-    float worst = 0;
-    for (int d = 0; d < n; ++d) {
-      RK(cudaSetDevice(d)); RK(cudaDeviceSynchronize());
-      float ms; RK(cudaEventElapsedTime(&ms, e0[d], e1[d])); if (ms > worst) worst = ms;
-    }
-    printf("%-36s %8.1f us  %7.1f GB/s/GPU(chunk)\n", name, worst * 1e3 / it, (bytes / n) / (worst / it * 1e-3) / 1e9);
-  };
+  for (int d = 0; d < n; ++d) {
+    RK(cudaSetDevice(d));
+    RK(cudaMalloc(&sink[d], 64));
+    RK(cudaMalloc(&fl[d], flush_n * 16));
+    RK(cudaStreamCreate(&st[d]));
+  }
+  printf("%d GPUs, message %zu MiB, chunk %zu MiB; L2 flushed before each iteration; time = max over GPUs, median of 7\n",
+         n, bytes >> 20, (bytes / n) >> 20);
+  printf("%-44s %9s %10s %10s\n", "kernel", "us", "busBW", "link/dir");
   const size_t chunk = bytes / n;
-  for (int grid : {148, 296, 592, 1184})
-    for (int thr : {256, 512}) {
-      char nm[64];
-      snprintf(nm, 64, "ld_reduce U4 grid %d x %d", grid, thr);
-      run(nm, [&](int d) { k_ldred<4><<<grid, thr, 0, st[d]>>>((char*)mcva[d], d * chunk, (d + 1) * chunk, sink[d]); });
-      snprintf(nm, 64, "ld_reduce U8 grid %d x %d", grid, thr);
-      run(nm, [&](int d) { k_ldred<8><<<grid, thr, 0, st[d]>>>((char*)mcva[d], d * chunk, (d + 1) * chunk, sink[d]); });
-      snprintf(nm, 64, "st U4 grid %d x %d", grid, thr);
-      run(nm, [&](int d) { k_st<4><<<grid, thr, 0, st[d]>>>((char*)mcva[d], d * chunk, (d + 1) * chunk); });
-      snprintf(nm, 64, "ld_reduce+st U4 grid %d x %d", grid, thr);
-      run(nm, [&](int d) { k_both<4><<<grid, thr, 0, st[d]>>>((char*)mcva[d], d * chunk, (d + 1) * chunk); });
+  auto run = [&](const char* name, int mode, auto launch) {
+    std::vector<float> ts;
+    cudaEvent_t e0[8], e1[8];
+    for (int d = 0; d < n; ++d) { RK(cudaSetDevice(d)); RK(cudaEventCreate(&e0[d])); RK(cudaEventCreate(&e1[d])); }
+    for (int it = 0; it < 9; ++it) {
+      for (int d = 0; d < n; ++d) { RK(cudaSetDevice(d)); k_flush<<<592, 512, 0, st[d]>>>(fl[d], flush_n, (float)it); }
+      for (int d = 0; d < n; ++d) { RK(cudaSetDevice(d)); RK(cudaStreamSynchronize(st[d])); }
+      for (int d = 0; d < n; ++d) {
+        RK(cudaSetDevice(d));
+        RK(cudaEventRecord(e0[d], st[d]));
+        launch(d);
+        RK(cudaEventRecord(e1[d], st[d]));
+      }
+      float worst = 0;
+      for (int d = 0; d < n; ++d) {
+        RK(cudaSetDevice(d)); RK(cudaStreamSynchronize(st[d]));
+        float ms; RK(cudaEventElapsedTime(&ms, e0[d], e1[d])); worst = std::max(worst, ms);
+      }
+      if (it >= 2) ts.push_back(worst);
     }
+    std::sort(ts.begin(), ts.end());
+    const double t = ts[ts.size() / 2] * 1e-3;
+    // all-reduce busBW convention 2(N-1)/N * S / t; per-direction link bytes of the body (N+1)/N * S
+    const double bus = (mode == 2 ? 2.0 * (n - 1) / n * bytes / t : 0) / 1e9;
+    const double link = (mode == 0 ? bytes : mode == 1 ? bytes : (double)(n + 1) / n * bytes) / t / 1e9;
+    printf("%-44s %9.1f %10.1f %10.1f\n", name, t * 1e6, bus, link);
+  };
+#define RUN(MODE, U, WEAK, G, T)                                                                       \
+  {                                                                                                    \
+    char nm[64];                                                                                       \
+    snprintf(nm, 64, "%s U%d %s grid %dx%d", MODE == 0 ? "ld_reduce" : MODE == 1 ? "st" : "ldred+st", U, \
+             WEAK ? "weak" : "sys", G, T);                                                             \
+    run(nm, MODE, [&](int d) {                                                                         \
+      k_body<MODE, U, WEAK><<<G, T, 0, st[d]>>>((char*)mcva[d], d * chunk, (d + 1) * chunk, sink[d]); \
+    });                                                                                                \
+  }
+  RUN(0, 4, false, 148, 512) RUN(1, 4, false, 148, 512)
+  RUN(2, 1, true, 148, 128) RUN(2, 2, true, 148, 128) RUN(2, 4, true, 148, 128)
+  RUN(2, 1, true, 148, 256) RUN(2, 2, true, 148, 256)
+  RUN(2, 1, true, 148, 384) RUN(2, 1, true, 148, 512) RUN(2, 1, true, 148, 768) RUN(2, 1, true, 148, 1024)
+  RUN(2, 1, true, 74, 512) RUN(2, 1, true, 74, 1024) RUN(2, 1, true, 296, 256) RUN(2, 1, true, 296, 128)
+  RUN(2, 2, true, 74, 512) RUN(2, 4, true, 74, 256) RUN(2, 1, true, 444, 256)
   return 0;
 }

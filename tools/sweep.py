@@ -56,6 +56,11 @@ def main():
     count_max = maxb // 4
     bufs = [torch.randn(count_max, device=dev) for _ in range(reps)]
     outs = [torch.empty(n * count_max if "all_gather" in a.ops else count_max, device=dev) for _ in range(reps)]
+    nvls_buf = None
+    if "nvls" in a.algos.split(",") and world > 1:  # in-switch reduction: in place in the multicast region
+        comm.enable_nvls(maxb + (4 << 20))
+        nvls_buf = comm.alloc_nvls(count_max, torch.float32)
+        nvls_buf.copy_(bufs[0])
 
     def tmax(x):
         if world == 1:
@@ -79,6 +84,11 @@ def main():
                     os_ = [o[:count] for o in outs]
                     if world == 1:
                         fn = lambda: comm.all_reduce(xs, "sum", outs=os_, algo=algo)  # noqa: E731
+                    elif algo == "nvls":
+                        if nvls_buf is None:
+                            continue
+                        fn = lambda: comm.all_reduce_tensor(nvls_buf[:count], "mean", out=nvls_buf[:count],  # noqa: E731
+                                                            algo="nvls")
                     else:
                         fn = lambda: comm.all_reduce_tensor(xs[0], "sum", out=os_[0], algo=algo)  # noqa: E731
                     factor = 2.0 * (n - 1) / n
