@@ -153,6 +153,26 @@ RP_API int rp_nvls_pool(rp_comm_t comm, void** base, size_t* bytes);
 RP_API int rp_all_reduce(rp_comm_t comm, const void* src, void* dst, size_t count, int dtype_in,
                   int dtype_comm, int dtype_out, int op, int algo, void* stream);
 
+/* ---- fused optimizer apply (wrap_optimizer as one kernel) ------------------- */
+/* The wrapped optimizer's step in ONE
+ * kernel: the gradient bucket `grad` (count elements of dtype_grad, f32|bf16) is
+ * averaged with the rank-ordered premean fold (bit-identical to rp_all_reduce
+ * RP_PREMEAN), the rank owning each chunk applies the optimizer update to the f32
+ * parameter bucket `param` (count elements) in f32, and stores the updated values
+ * into every rank's `param` -- every replica ends with the same bits (mirrored
+ * variables). Both buckets are pool-resident at symmetric offsets.
+ * Optimizer state covers this rank's shard only (rp_apply_shard); `step` is a
+ * device int32 the kernel reads and advances (graph-replay safe).
+ * hyper[6] = {lr, momentum | beta1, dampening | beta2, weight_decay, eps, nesterov}
+ * with torch.optim.SGD / Adam / AdamW semantics (non-amsgrad, not maximize). */
+enum { RP_OPT_SGD = 0, RP_OPT_ADAM = 1, RP_OPT_ADAMW = 2 };
+RP_API int rp_apply_shard(rp_comm_t comm, size_t count, int dtype_grad, size_t* first, size_t* len);
+RP_API int rp_all_reduce_apply(rp_comm_t comm, const void* grad, void* param, size_t count, int dtype_grad, int opt,
+                               const double* hyper, float* state0, float* state1, int32_t* step, void* stream);
+RP_API int rp_all_reduce_apply_v(rp_comm_t comm, const void* const* grad, void* const* param, size_t count,
+                                 int dtype_grad, int opt, const double* hyper, float* const* state0,
+                                 float* const* state1, int32_t* const* step, void* stream);
+
 /* The algorithm rp_all_reduce would run for these arguments (RP_ALGO_ONESHOT,
  * RP_ALGO_TWOSHOT or RP_ALGO_NVLS) in *chosen; nothing is launched. */
 RP_API int rp_all_reduce_algo(rp_comm_t comm, const void* src, const void* dst, size_t count, int dtype_in,

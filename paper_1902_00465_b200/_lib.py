@@ -24,6 +24,8 @@ OPS = {"sum": SUM, "mean": MEAN, "max": MAX, "premean": PREMEAN}
 AUTO, ONESHOT, TWOSHOT = 0, 1, 2
 DIRECT, SCATTER = 1, 2
 NVLS = 3
+# fused optimizer apply (rp_all_reduce_apply)
+OPT_SGD, OPT_ADAM, OPT_ADAMW = 0, 1, 2
 ALGOS = {"auto": AUTO, "oneshot": ONESHOT, "twoshot": TWOSHOT, "direct": DIRECT, "scatter": SCATTER, "nvls": NVLS}
 # layouts
 NHWC, NCHW = 0, 1
@@ -64,6 +66,11 @@ SIGNATURES = {
     "rp_all_reduce": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _i, _i, _i, _c_void_p]),
     "rp_all_gather": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _c_void_p]),
     "rp_broadcast": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _c_void_p]),
+    "rp_apply_shard": (_i, [_c_void_p, _size_t, _i, ctypes.POINTER(_size_t), ctypes.POINTER(_size_t)]),
+    "rp_all_reduce_apply": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, ctypes.POINTER(_d), _c_void_p,
+                                 _c_void_p, _c_void_p, _c_void_p]),
+    "rp_all_reduce_apply_v": (_i, [_c_void_p, _pp, _pp, _size_t, _i, _i, ctypes.POINTER(_d), _pp, _pp, _pp,
+                                   _c_void_p]),
     "rp_all_reduce_algo": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _i, _i, _i,
                                 ctypes.POINTER(ctypes.c_int)]),
     "rp_all_reduce_v": (_i, [_c_void_p, _pp, _pp, _size_t, _i, _i, _i, _i, _i, _c_void_p]),

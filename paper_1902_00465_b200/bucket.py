@@ -25,7 +25,8 @@ _ALIGN_ELEMS = 64  # keep every tensor's slot 128-byte aligned for 16-bit types
 
 
 class _Bucket:
-    def __init__(self, comm, params_per_replica, grad_dtype, comm_dtype):
+    def __init__(self, comm, params_per_replica, grad_dtype, comm_dtype, allow_nvls: bool = True,
+                 match_param_layout: bool = False):
         self.comm = comm
         self.grad_dtype = grad_dtype
         self.comm_dtype = comm_dtype
@@ -38,7 +39,8 @@ class _Bucket:
         self.offs = offs
         self.numel = o
         esz = torch.empty((), dtype=comm_dtype).element_size()
-        if isinstance(comm, Communicator) and comm.nvls_free >= o * esz + 256:
+        self.match_param_layout = match_param_layout
+        if allow_nvls and isinstance(comm, Communicator) and comm.nvls_free >= o * esz + 256:
             buf = comm.alloc_nvls(o, comm_dtype)  # reduced inside the NVSwitch (rp.h RP_ALGO_NVLS)
         else:
             buf = comm.alloc(o, comm_dtype)
@@ -57,24 +59,32 @@ class _Bucket:
             if p.grad is None:
                 p.grad = torch.zeros_like(p)
             g = p.grad
-            if not _is_dense(g):
+            if not _is_dense(g) or (self.match_param_layout and g.stride() != p.stride()):
                 d = torch.empty_like(p)
                 d.copy_(g)
                 p.grad = g = d
             out.append(g)
         return out
 
-    def reduce(self, kind: str):
+    def pack(self):
+        """Every replica's gradients -> its flat bucket (one multi-tensor launch each,
+        with the exchange cast fused). Returns the gradient lists (for unpack)."""
         lib = _lib.load()
         stream = torch.cuda.current_stream(self.flat[0].device).cuda_stream
         gcode, ccode = dtype_code(self.grad_dtype), dtype_code(self.comm_dtype)
         grads = [self._grads(r) for r in range(len(self.params))]
-        keep = []
         for r, flat in enumerate(self.flat):
             pp, k = _lib.ptr_array([g.data_ptr() for g in grads[r]])
-            keep.append(k)
             _lib.check(lib.rp_pack(flat.data_ptr(), ccode, pp, self._counts_c[0], self._offs_c[0], len(grads[r]),
                                    gcode, stream), "pack")
+        return grads
+
+    def reduce(self, kind: str):
+        lib = _lib.load()
+        stream = torch.cuda.current_stream(self.flat[0].device).cuda_stream
+        gcode, ccode = dtype_code(self.grad_dtype), dtype_code(self.comm_dtype)
+        grads = self.pack()
+        keep = []
         if isinstance(self.comm, VirtualCommunicator):
             self.comm.all_reduce(self.flat, kind, outs=self.flat)
         else:

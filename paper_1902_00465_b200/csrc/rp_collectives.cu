@@ -273,6 +273,15 @@ void base_args(rp_comm* c, CollArgs& a) {
 
 }  // namespace
 
+// shared with rp_apply.cu (fused optimizer apply)
+bool rp_symmetric_in_pool(rp_comm* c, const void* const* ptrs, size_t bytes, size_t* off) {
+  return symmetric_in_pool(c, ptrs, bytes, off);
+}
+void rp_base_args(rp_comm* c, CollArgs& a) { base_args(c, a); }
+int rp_dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, const char* tag) {
+  return dyn_launch(c, fn, a, stream, tag, 0, kThreads, 0);
+}
+
 // Algorithm choice: deterministic in (arguments, world, NVLS placement), hence
 // identical on every rank (NVLS buffers are allocated symmetrically).
 int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,

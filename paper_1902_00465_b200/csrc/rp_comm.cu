@@ -424,6 +424,27 @@ int rp_all_reduce(rp_comm_t c, const void* src, void* dst, size_t count, int dty
   return rp_launch_all_reduce(c, s, d, count, dtype_in, dtype_comm, dtype_out, op, algo, (cudaStream_t)stream);
 }
 
+int rp_all_reduce_apply(rp_comm_t c, const void* grad, void* param, size_t count, int dtype_grad, int opt,
+                        const double* hyper, float* state0, float* state1, int32_t* step, void* stream) {
+  RP_REQUIRE_READY(c, "rp_all_reduce_apply");
+  if (c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_all_reduce_apply: virtual communicator needs rp_all_reduce_apply_v");
+  const void* g[1] = {grad};
+  void* p[1] = {param};
+  float* s0[1] = {state0};
+  float* s1[1] = {state1};
+  int32_t* st[1] = {step};
+  return rp_launch_apply(c, g, p, count, dtype_grad, opt, hyper, s0, s1, st, (cudaStream_t)stream);
+}
+
+int rp_all_reduce_apply_v(rp_comm_t c, const void* const* grad, void* const* param, size_t count, int dtype_grad,
+                          int opt, const double* hyper, float* const* state0, float* const* state1,
+                          int32_t* const* step, void* stream) {
+  RP_REQUIRE_READY(c, "rp_all_reduce_apply_v");
+  if (!c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_all_reduce_apply_v: needs a virtual communicator");
+  if (!grad || !param) return rp_fail(RP_ERR_INVALID, "rp_all_reduce_apply_v: NULL argument");
+  return rp_launch_apply(c, grad, param, count, dtype_grad, opt, hyper, state0, state1, step, (cudaStream_t)stream);
+}
+
 int rp_all_reduce_algo(rp_comm_t c, const void* src, const void* dst, size_t count, int dtype_in, int dtype_comm,
                        int dtype_out, int op, int algo, int* chosen) {
   RP_REQUIRE_READY(c, "rp_all_reduce_algo");

@@ -153,6 +153,16 @@ int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, 
 // Blocks per rank for a collective kernel given its per-block occupancy.
 int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want);
 
+// shared collective plumbing (rp_collectives.cu), used by rp_apply.cu. The
+// dynamically scheduled launch passes &a as the kernel's only parameter: a kernel
+// taking a larger struct whose FIRST member is the CollArgs gets the whole struct.
+bool rp_symmetric_in_pool(rp_comm* c, const void* const* ptrs, size_t bytes, size_t* off);
+void rp_base_args(rp_comm* c, CollArgs& a);
+int rp_dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, const char* tag);
+int rp_launch_apply(rp_comm* c, const void* const* grad, void* const* param, size_t count, int dtype_grad, int opt,
+                    const double* hyper, float* const* state0, float* const* state1, int32_t* const* step,
+                    cudaStream_t stream);
+
 // NVLS (rp_nvls.cu)
 void rp_nvls_destroy(rp_comm* c);
 // [p, p + bytes) lies in this rank's bound NVLS region, 16-byte aligned

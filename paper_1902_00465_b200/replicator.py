@@ -251,9 +251,13 @@ class Replicator:
                     if self.comm.world > 1:
                         self.comm.broadcast_tensor(tensors[0][k].data, root=0)
 
-    def wrap_optimizer(self, optimizer, kind: str = "premean") -> "ReplicatedOptimizer":
+    def wrap_optimizer(self, optimizer, kind: str = "premean", fused: bool = False):
         """apply_gradients first averages every gradient across
-        replicas with all_sum(g / R), then applies the base rule."""
+        replicas with all_sum(g / R), then applies the base rule.
+
+        ``fused=True`` (torch.optim.SGD / Adam / AdamW, f32 parameters): the
+        average and the update run as one kernel that updates each rank's shard and
+        stores the new parameters on every replica (fused.py, csrc/rp_apply.cu)."""
         if isinstance(optimizer, PerReplica):
             opts = list(optimizer.values)
         else:
@@ -261,6 +265,11 @@ class Replicator:
         if self.is_virtual and len(opts) != self.comm.world and self.comm.world > 1:
             raise errors.ConfigurationError("virtual replicas need one optimizer per replica "
                                             "(repl.replicate(lambda: make_opt(...)))")
+        if fused:
+            if kind != "premean":
+                raise errors.ConfigurationError("fused apply averages with the premean fold")
+            from .fused import FusedReplicatedOptimizer
+            return FusedReplicatedOptimizer(self, opts)
         return ReplicatedOptimizer(self, opts, kind)
 
     # -- run ----------------------------------------------------------------

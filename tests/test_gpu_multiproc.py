@@ -386,6 +386,78 @@ def body_wrap_nvls(rank, world):
     repl.comm.close()
 
 
+def body_fused_apply(rank, world):
+    """wrap_optimizer(Adam, fused=True) over real ranks: each step equals torch's
+    Adam driven by the rank-ordered averaged gradient (gathered and folded by the
+    oracle), replicas stay bit-identical, and the whole training step (forward,
+    backward, fused apply) replays from a CUDA graph."""
+    from oracle import collectives as O
+    from paper_1902_00465_b200.replicator import Replicator
+
+    dev = torch.device(f"cuda:{rank}")
+    repl = Replicator(device=rank, pool_bytes=32 << 20)
+    torch.manual_seed(rank)
+    with repl.context():
+        model = repl.replicate(lambda: torch.nn.Sequential(torch.nn.Linear(784, 256), torch.nn.ReLU(),
+                                                           torch.nn.Linear(256, 10)))
+        opt = repl.wrap_optimizer(torch.optim.Adam(model.parameters(), lr=1e-3, weight_decay=1e-4), fused=True)
+    ref = torch.nn.Sequential(torch.nn.Linear(784, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).to(dev)
+    with torch.no_grad():
+        for p, q in zip(ref.parameters(), model.local.parameters()):
+            p.copy_(q)
+    ref_opt = torch.optim.Adam(ref.parameters(), lr=1e-3, weight_decay=1e-4)
+    B = 16
+    for step in range(3):
+        g = torch.Generator().manual_seed(step)
+        xs = torch.randn(world * B, 784, generator=g).to(dev)
+        ys = torch.randint(0, 10, (world * B,), generator=g).to(dev)
+        opt.zero_grad()
+        torch.nn.functional.cross_entropy(model(xs[rank * B:(rank + 1) * B]), ys[rank * B:(rank + 1) * B]).backward()
+        flat = torch.cat([p.grad.reshape(-1) for p in model.local.parameters()])
+        every = repl.comm.all_gather_tensor(flat).cpu().numpy()
+        avg = torch.from_numpy(O.fold_premean([every[r] for r in range(world)])).to(dev)
+        o = 0
+        for p in ref.parameters():
+            p.grad = avg[o:o + p.numel()].view_as(p).clone()
+            o += p.numel()
+        opt.step()
+        ref_opt.step()
+    for p, q in zip(model.local.parameters(), ref.parameters()):
+        assert torch.allclose(p, q, rtol=2e-6, atol=2e-7), (p - q).abs().max().item()
+    flat = torch.cat([p.detach().reshape(-1) for p in model.local.parameters()])
+    gathered = repl.comm.all_gather_tensor(flat)
+    assert all(torch.equal(gathered[r], gathered[0]) for r in range(world))
+    # the whole step in a CUDA graph (device-side step counter and sequencing state)
+    x = torch.randn(B, 784, device=dev, generator=torch.Generator(device=dev).manual_seed(50 + rank))
+    y = torch.randint(0, 10, (B,), device=dev, generator=torch.Generator(device=dev).manual_seed(60 + rank))
+
+    def train_step():
+        opt.zero_grad()
+        torch.nn.functional.cross_entropy(model(x), y).backward()
+        opt.step()
+
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        train_step()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        train_step()
+    before = flat.clone()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    repl.comm.check()
+    assert int(opt.groups[0].steps[0].item()) == 3 + 1 + 3
+    flat = torch.cat([p.detach().reshape(-1) for p in model.local.parameters()])
+    assert not torch.equal(flat, before)
+    gathered = repl.comm.all_gather_tensor(flat)
+    assert all(torch.equal(gathered[r], gathered[0]) for r in range(world))
+    repl.comm.close()
+
+
 def body_graph(rank, world):
     """Each rank captures the same sequence of collectives in a CUDA graph and
     replays it; device-side sequencing keeps the ranks in step across replays."""
@@ -474,6 +546,10 @@ def test_nvls_all_reduce_multiprocess():
 
 def test_wrap_optimizer_nvls_buckets_multiprocess():
     run_world("body_wrap_nvls")
+
+
+def test_fused_apply_multiprocess():
+    run_world("body_fused_apply")
 
 
 def test_cuda_graph_replay_multiprocess():
