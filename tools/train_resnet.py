@@ -36,6 +36,10 @@ def main():
     p.add_argument("--out", default=None)
     p.add_argument("--no-average", action="store_true", help="control run: skip the gradient all-reduce")
     p.add_argument("--diagnose", action="store_true", help="print per-phase GPU/host times of 8 steps")
+    p.add_argument("--fused", action="store_true",
+                   help="wrap_optimizer(fused=True): average + SGD update of each rank's shard in one kernel")
+    p.add_argument("--nvls", action="store_true",
+                   help="place the gradient buckets in an NVSwitch multicast region (in-switch reduction at >= 4)")
     a = p.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -52,12 +56,13 @@ def main():
     torch.backends.cuda.matmul.allow_tf32 = True
     torch.backends.cudnn.allow_tf32 = True
     repl = Replicator(device=local, pool_bytes=512 << 20,
-                      grad_comm_dtype=torch.bfloat16 if a.grad_comm == "bf16" else None)
+                      grad_comm_dtype=torch.bfloat16 if a.grad_comm == "bf16" else None,
+                      nvls_bytes=(128 << 20) if (a.nvls and world > 1) else 0)
     torch.manual_seed(rank)  # replicate() broadcasts replica 0's init
     with repl.context():
         model = repl.replicate(lambda: torchvision.models.resnet50().to(memory_format=torch.channels_last))
         opt = repl.wrap_optimizer(torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, nesterov=True,
-                                                  weight_decay=1e-4))
+                                                  weight_decay=1e-4), fused=a.fused)
     net = model.local
     if a.no_average:
         opt.average_gradients = lambda: None
@@ -118,13 +123,15 @@ def main():
     # the gradient all-reduce alone (same buckets), for its share of the step
     ar_ms = 0.0
     if world > 1 and not a.no_average:
-        bk = opt._buckets
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         torch.distributed.barrier()
         a0.record(stream)
         for _ in range(10):
-            bk.reduce("premean")
+            if a.fused:  # pack + fused average/update (the whole optimizer step)
+                opt._apply_all()
+            else:
+                opt._buckets.reduce("premean")
         a1.record(stream)
         torch.cuda.synchronize()
         ar_ms = a0.elapsed_time(a1) / 10
@@ -137,12 +144,15 @@ def main():
     gathered = repl.all_gather(flat) if world > 1 else flat.unsqueeze(0)
     consistent = bool(all(torch.equal(gathered[r], gathered[0]) for r in range(world)))
     if rank == 0:
-        grad_bytes = sum(b.numel * b.flat[0].element_size() for b in opt._buckets.buckets) if opt._buckets else 0
+        if a.fused:
+            grad_bytes = sum(g.grads.numel * g.grads.flat[0].element_size() for g in opt.groups if g is not None)
+        else:
+            grad_bytes = sum(b.numel * b.flat[0].element_size() for b in opt._buckets.buckets) if opt._buckets else 0
         line = {"metric": "ResNet-50 synthetic img/s", "value": world * a.batch / (ms / 1e3), "unit": "img/s",
                 "n_gpus": world, "per_gpu_batch": a.batch, "ms_per_step": ms, "steps": a.steps, "warmup": a.warmup,
                 "allreduce_ms": ar_ms, "allreduce_share": ar_ms / ms if ms else 0.0,
                 "grad_exchange_bytes": grad_bytes, "grad_comm": a.grad_comm, "replicas_identical": consistent,
-                "loss": float(loss.item()), "wall_s": wall,
+                "loss": float(loss.item()), "wall_s": wall, "fused_apply": a.fused, "nvls": a.nvls,
                 "config": {"model": "resnet50 (torchvision, random init)", "input": "synthetic 224x224x3 channels_last",
                            "precision": "bf16 autocast, fp32 master", "optimizer": "SGD nesterov 0.9 wd 1e-4"}}
         print(json.dumps(line), flush=True)
