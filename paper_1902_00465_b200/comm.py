@@ -282,6 +282,33 @@ class Communicator(_Base):
                    "all_reduce_algo")
         return {1: "oneshot", 2: "twoshot", 3: "nvls"}[chosen.value]
 
+    def all_gather_ragged(self, x: torch.Tensor) -> list[torch.Tensor]:
+        """shapes may differ across ranks in the leading dimension
+        only. Two exchanges through the all_gather kernel: (leading dim, digest of the
+        trailing shape and dtype), then every rank's rows padded to the longest;
+        returns [t_0, ..., t_{N-1}] in rank order (views of one gathered buffer)."""
+        x = _contig_cuda(x, self.device)
+        if x.dim() == 0:
+            x = x.reshape(1)
+        tail = hashlib.sha256(repr((tuple(x.shape[1:]), str(x.dtype))).encode()).digest()[:8]
+        meta = torch.tensor([x.shape[0], int.from_bytes(tail, "little", signed=True)], dtype=torch.int64)
+        g = self.all_gather_tensor(meta.to(x.device)).cpu()
+        for r in range(self.world):
+            if int(g[r, 1]) != int(g[self.rank, 1]):
+                raise errors.ProtocolError(f"all_gather: rank {r} and rank {self.rank} differ beyond the leading "
+                                           f"dimension (local {tuple(x.shape)}, {x.dtype})")
+        lens = [int(g[r, 0]) for r in range(self.world)]
+        m = max(lens)
+        if m == x.shape[0]:
+            xp = x
+        else:
+            xp = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+            xp[: x.shape[0]] = x
+        if m == 0:
+            return [xp[:0] for _ in range(self.world)]
+        out = self.all_gather_tensor(xp)
+        return [out[r, : lens[r]] for r in range(self.world)]
+
     def all_gather_tensor(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """out[r] = x of rank r; out has shape (world,) + x.shape."""
         x = _contig_cuda(x, self.device)
@@ -318,14 +345,20 @@ class Communicator(_Base):
         return wrap(y.cpu().numpy())
 
     def all_gather(self, local, label=None):
+        """[t_0, ..., t_{N-1}] in rank order; leading dimensions may differ across
+        ranks, scalars stay scalars."""
         self._use_label(label)
         if isinstance(local, torch.Tensor):
-            g = self.all_gather_tensor(local)
-            return [g[r] for r in range(self.world)]
+            if local.dim() == 0:
+                g = self.all_gather_tensor(local.reshape(1))
+                return [g[r, 0] for r in range(self.world)]
+            return self.all_gather_ragged(local)
         arr, wrap = _host_in(local)
         x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
-        g = self.all_gather_tensor(x).cpu().numpy()
-        return [wrap(g[r]) for r in range(self.world)]
+        if x.dim() == 0:
+            g = self.all_gather_tensor(x.reshape(1)).cpu().numpy()
+            return [wrap(g[r, 0]) for r in range(self.world)]
+        return [wrap(t.cpu().numpy()) for t in self.all_gather_ragged(x)]
 
     def broadcast(self, root_value, label=None, shape=None, dtype=None, root: int = 0):
         """Reference form (graph.py:580-582): root passes its value, others pass None
@@ -351,17 +384,27 @@ class Communicator(_Base):
         return wrap(y.cpu().numpy())
 
     # -- protocol agreement (debug): every rank must issue the same collective
-    def verify(self, label: str, kind: str, shape, dtype) -> None:
-        """All ranks exchange a digest of (label, kind, shape, dtype) through this
-        communicator's own all_gather and raise ProtocolError naming the first
-        disagreeing rank."""
-        h = hashlib.sha256(repr((label, kind, tuple(shape), str(dtype))).encode()).digest()[:16]
+    def verify(self, label: str, kind: str, shape, dtype, position=None) -> None:
+        """All ranks exchange a digest of (position, label, kind, shape, dtype)
+        through this communicator's own all_gather and raise ProtocolError naming
+        the disagreeing ranks and what each issued.
+        ``position`` is the call's (generation, index): a different ORDER of the
+        same calls is caught too."""
+        desc = repr((position, label, kind, tuple(shape), str(dtype)))
+        h = hashlib.sha256(desc.encode()).digest()[:16]
         t = torch.frombuffer(bytearray(h), dtype=torch.uint8).to(f"cuda:{self.device}")
         g = self.all_gather_tensor(t).cpu()
-        for r in range(self.world):
-            if not torch.equal(g[r], g[self.rank]):
-                raise errors.ProtocolError(
-                    f"rank {r} and rank {self.rank} disagree on collective {label!r} ({kind}, {tuple(shape)})")
+        bad = [r for r in range(self.world) if not torch.equal(g[r], g[self.rank])]
+        if bad:
+            # second exchange (every rank takes this branch: some rank disagrees with
+            # each of them): the descriptions themselves, for the message
+            raw = desc.encode()[:240]
+            buf = torch.zeros(256, dtype=torch.uint8)
+            buf[: len(raw)] = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+            d = self.all_gather_tensor(buf.to(f"cuda:{self.device}")).cpu()
+            other = bytes(d[bad[0]].numpy()).rstrip(b"\0").decode(errors="replace")
+            raise errors.ProtocolError(f"collective protocol mismatch: rank {self.rank} issued {desc}, "
+                                       f"rank {bad[0]} issued {other} (ranks {bad} disagree with rank {self.rank})")
 
 
 class VirtualCommunicator(_Base):
@@ -431,6 +474,33 @@ class VirtualCommunicator(_Base):
         _lib.check(self._lib.rp_all_gather_v(self._handle, sp, dp, xs[0].numel() * xs[0].element_size(),
                                              _stream_handle(self.device)), "all_gather")
         return outs
+
+    def all_gather_ragged(self, xs):
+        """leading dimensions may differ across replicas. Returns, for
+        every replica, the list [x_0, ..., x_{R-1}] (views of its gathered buffer)."""
+        if len(xs) != self.world:
+            raise errors.ShapeError(f"expected {self.world} replica tensors, got {len(xs)}")
+        xs = [_contig_cuda(x, self.device) for x in xs]
+        xs = [x.reshape(1) if x.dim() == 0 else x for x in xs]
+        tail = (tuple(xs[0].shape[1:]), xs[0].dtype)
+        for r, x in enumerate(xs):
+            if (tuple(x.shape[1:]), x.dtype) != tail:
+                raise errors.ProtocolError(f"all_gather: replica {r} differs beyond the leading dimension: "
+                                           f"{tuple(x.shape)}/{x.dtype} vs {tuple(xs[0].shape)}/{xs[0].dtype}")
+        lens = [x.shape[0] for x in xs]
+        m = max(lens)
+        if m == 0:
+            return [[x[:0] for x in xs] for _ in xs]
+        padded = []
+        for x in xs:
+            if x.shape[0] == m:
+                padded.append(x)
+            else:
+                p = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+                p[: x.shape[0]] = x
+                padded.append(p)
+        outs = self.all_gather(padded)
+        return [[o[q, : lens[q]] for q in range(self.world)] for o in outs]
 
     def broadcast(self, xs, root=0, outs=None, algo="auto", label=None):
         self._use_label(label)

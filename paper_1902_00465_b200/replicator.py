@@ -156,6 +156,25 @@ class _AllReduceFn(torch.autograd.Function):
 # Replicator
 # ---------------------------------------------------------------------------
 
+class DriverValue:
+    """Result of map_gather / map_reduce: delivered to the driver.
+    Reading ``.value`` inside a replicated step raises EvaluationError (the SPEC's
+    "consuming the result inside a replica" error)."""
+
+    def __init__(self, value):
+        self._value = value
+
+    @property
+    def value(self):
+        if getattr(_tls, "in_step", False):
+            raise errors.EvaluationError("map_gather/map_reduce results are delivered to the driver: read them "
+                                         "after Replicator.run returns (SPEC.md:223-231)")
+        return self._value
+
+    def __repr__(self):
+        return "DriverValue(<delivered to the driver>)"
+
+
 class Replicator:
     """Synchronous data-parallel Replicator (Table 1 MultiGpu/MultiWorker kinds,
     PAPER.md:150-160) whose collectives are NVLink peer-memory kernels."""
@@ -163,11 +182,17 @@ class Replicator:
     def __init__(self, num_replicas: int | None = None, *, group=None, device: int | None = None,
                  pool_bytes: int = DEFAULT_POOL_BYTES, timeout_s: float = 20.0,
                  grad_comm_dtype: torch.dtype | None = None, bucket_bytes: int | None = None,
-                 nvls_bytes: int = 0):
+                 nvls_bytes: int = 0, check_protocol: bool = False):
         """``nvls_bytes`` > 0 (multi-process, >= 2 ranks): bind that much memory per
         rank to an NVSwitch multicast region and place gradient fusion buckets in it
         while it has room, so wrap_optimizer's reduction runs in the switch
-        (RP_ALGO_NVLS; not rank-ordered -- leave 0 for bit-exact reference parity)."""
+        (RP_ALGO_NVLS; not rank-ordered -- leave 0 for bit-exact reference parity).
+
+        ``check_protocol`` (debug): every collective first
+        checks that all ranks issue the same (generation, call index, label, kind,
+        shape, dtype) and that no label repeats within a generation (one
+        generation per ``run``/``new_generation``), raising ProtocolError naming the
+        ranks. Virtual replicas are always checked by the rendezvous."""
         import torch.distributed as dist
 
         mp = dist.is_available() and dist.is_initialized()
@@ -187,6 +212,9 @@ class Replicator:
             self.kind = "non" if n == 1 else "multi_device"
             self._rv = _Rendezvous(n)
         self.device = self.comm.device
+        self.check_protocol = check_protocol
+        self.comm.check_labels = check_protocol
+        self._generation, self._call_index = 0, 0
         self.grad_comm_dtype = grad_comm_dtype
         self.bucket_bytes = bucket_bytes
         self._in_context = False
@@ -285,8 +313,13 @@ class Replicator:
                 inp = input_fn(r)
                 if callable(inp):
                     inp = inp()
-            return step_fn(inp) if input_fn is not None else step_fn()
+            _tls.in_step = True
+            try:
+                return step_fn(inp) if input_fn is not None else step_fn()
+            finally:
+                _tls.in_step = False
 
+        self.new_generation()
         if self.comm.world == 1 or not self.is_virtual:
             _tls.replica = 0
             if self.is_virtual:
@@ -319,6 +352,21 @@ class Replicator:
     def _collective(self, desc, x, fn_virtual):
         return self._rv(self.replica_id, desc, x, fn_virtual)
 
+    def new_generation(self) -> None:
+        """Start a new generation (training step): labels may repeat."""
+        self._generation += 1
+        self._call_index = 0
+        self.comm.new_generation()
+
+    def _verify(self, label, kind, shape, dtype):
+        """check_protocol on a multi-process replicator: all ranks must be issuing
+        the same collective at the same position of the generation."""
+        if not self.check_protocol or self.is_virtual or self.comm.world == 1:
+            return
+        self.comm._use_label(label)
+        self.comm.verify(label, kind, shape, dtype, position=(self._generation, self._call_index))
+        self._call_index += 1
+
     def all_reduce(self, x: torch.Tensor, kind: str = "sum", label: str | None = None) -> torch.Tensor:
         """Cross-replica fold of x (sum / mean / max / premean), ascending replica order."""
         if self.comm.world == 1:
@@ -326,18 +374,27 @@ class Replicator:
         if self.is_virtual:
             return self._collective(("all_reduce", label, kind, tuple(x.shape), x.dtype), x,
                                     lambda xs: self.comm.all_reduce(xs, kind))
+        self._verify(label, kind, x.shape, x.dtype)
         return _AllReduceFn.apply(x, self.comm, kind)
 
     def all_sum(self, x: torch.Tensor, label: str | None = None) -> torch.Tensor:
         return self.all_reduce(x, "sum", label)
 
-    def all_gather(self, x: torch.Tensor, label: str | None = None) -> torch.Tensor:
-        """Returns (R,) + x.shape: every replica's x in replica order."""
+    def all_gather(self, x: torch.Tensor, label: str | None = None, ragged: bool = False):
+        """Returns (R,) + x.shape: every replica's x in replica order. ``ragged=True``
+        (leading dimensions may differ across replicas) returns the list
+        [x_0, ..., x_{R-1}] instead."""
         if self.is_virtual:
             if self.comm.world == 1:
-                return x.unsqueeze(0).clone()
+                return [x.clone()] if ragged else x.unsqueeze(0).clone()
+            if ragged:
+                return self._collective(("all_gather_ragged", label, tuple(x.shape[1:]), x.dtype), x,
+                                        lambda xs: self.comm.all_gather_ragged(xs))
             return self._collective(("all_gather", label, tuple(x.shape), x.dtype), x,
                                     lambda xs: self.comm.all_gather(xs))
+        self._verify(label, "gather", x.shape[1:] if ragged else x.shape, x.dtype)
+        if ragged:
+            return self.comm.all_gather_ragged(x)
         return self.comm.all_gather_tensor(x)
 
     def broadcast(self, x: torch.Tensor, root: int = 0, label: str | None = None) -> torch.Tensor:
@@ -346,15 +403,20 @@ class Replicator:
                 return x.clone()
             return self._collective(("broadcast", label, root, tuple(x.shape), x.dtype), x,
                                     lambda xs: self.comm.broadcast(xs, root=root))
+        self._verify(label, f"broadcast(root={root})", x.shape, x.dtype)
         return self.comm.broadcast_tensor(x.clone(), root=root)
 
-    def map_gather(self, x: torch.Tensor) -> torch.Tensor:
-        """per-replica values collected for the driver (here: every
-        process receives them; replicas must not feed them back into the step)."""
-        return self.all_gather(x.detach())
+    def map_gather(self, x: torch.Tensor, label: str | None = None) -> "DriverValue":
+        """per-replica values collected to the driver; replicas get
+        nothing back. Returns a DriverValue whose ``.value`` (the list of every
+        replica's x in replica order; leading dimensions may differ) can be read
+        only outside the replicated step -- e.g. from Replicator.run's outputs."""
+        vals = self.all_gather(x.detach(), label=label, ragged=True)
+        return DriverValue(list(vals))
 
-    def map_reduce(self, x: torch.Tensor, kind: str = "sum") -> torch.Tensor:
-        return self.all_reduce(x.detach(), kind)
+    def map_reduce(self, x: torch.Tensor, kind: str = "sum", label: str | None = None) -> "DriverValue":
+        """the replicas' values folded (rank order) for the driver."""
+        return DriverValue(self.all_reduce(x.detach(), kind, label=label))
 
     def batch_norm(self, h: torch.Tensor, eps: float = 1e-5) -> torch.Tensor:
         """The paper's cross-replica batch norm listing with the

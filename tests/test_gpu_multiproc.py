@@ -458,6 +458,44 @@ def body_fused_apply(rank, world):
     repl.comm.close()
 
 
+def body_protocol(rank, world):
+    """Replicator(check_protocol=True): mismatched shapes or
+    order raise ProtocolError on EVERY rank, naming what each issued; a label reused
+    within a generation is rejected, across generations it is fine; the reference
+    duck type's all_gather accepts differing leading dimensions."""
+    from paper_1902_00465_b200 import errors
+    from paper_1902_00465_b200.replicator import Replicator
+
+    dev = torch.device(f"cuda:{rank}")
+    repl = Replicator(device=rank, pool_bytes=16 << 20, check_protocol=True)
+    x = torch.full((4,), float(rank + 1), device=dev)
+    assert repl.all_sum(x, label="a").tolist() == [float(sum(range(1, world + 1)))] * 4
+    try:
+        repl.all_sum(x, label="a")  # same label, same generation
+        raise AssertionError("label reuse was accepted")
+    except errors.ProtocolError:
+        pass
+    repl.new_generation()
+    repl.all_sum(x, label="a")  # next generation: fine
+    y = torch.zeros(3 + (rank == world - 1), device=dev)  # the last rank disagrees on the shape
+    try:
+        repl.all_sum(y, label="b")
+        raise AssertionError("shape disagreement was accepted")
+    except errors.ProtocolError as e:
+        assert "issued" in str(e) and f"rank {rank}" in str(e), str(e)
+    repl.new_generation()
+    # the duck type (graph.py:575-579) with ragged leading dimensions; scalars stay scalars
+    rows = torch.arange((rank + 1) * 3, dtype=torch.float32, device=dev).reshape(rank + 1, 3)
+    got = repl.comm.all_gather(rows)
+    assert [tuple(t.shape) for t in got] == [(r + 1, 3) for r in range(world)]
+    assert all(torch.equal(got[r], torch.arange((r + 1) * 3, dtype=torch.float32, device=dev).reshape(r + 1, 3))
+               for r in range(world))
+    sc = repl.comm.all_gather(np.float64(rank))
+    assert [float(np.asarray(v)) for v in sc] == [float(r) for r in range(world)]
+    repl.comm.check()
+    repl.comm.close()
+
+
 def body_graph(rank, world):
     """Each rank captures the same sequence of collectives in a CUDA graph and
     replays it; device-side sequencing keeps the ranks in step across replays."""
@@ -550,6 +588,10 @@ def test_wrap_optimizer_nvls_buckets_multiprocess():
 
 def test_fused_apply_multiprocess():
     run_world("body_fused_apply")
+
+
+def test_protocol_checks_and_ragged_gather_multiprocess():
+    run_world("body_protocol")
 
 
 def test_cuda_graph_replay_multiprocess():

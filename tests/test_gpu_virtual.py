@@ -553,3 +553,34 @@ def test_fused_apply_rejects_unsupported():
             repl.wrap_optimizer(PerReplica([torch.optim.SGD(params[r].parameters(), lr=0.1) for r in range(2)],
                                            repl), kind="sum", fused=True)
     repl.comm.close()
+
+
+@pytest.mark.gpu
+def test_ragged_all_gather_and_driver_values_virtual():
+    """SPEC.md:205-213 (leading dimensions may differ) and :223-231 (map_gather /
+    map_reduce are delivered to the driver; reading them inside a replica fails)."""
+    n = 3
+    repl = Replicator(num_replicas=n, device=0, pool_bytes=16 << 20)
+
+    def step(x):
+        g = repl.all_gather(x, label="rows", ragged=True)
+        mg = repl.map_gather(x.sum(0), label="mg")
+        mr = repl.map_reduce(x.sum(), "sum", label="mr")
+        with pytest.raises(errors.EvaluationError):
+            _ = mr.value  # consumed inside the replicated step
+        return g, mg, mr
+
+    xs = [torch.arange(r * 4 + 1, dtype=torch.float32, device=DEV).repeat(2, 1).t().contiguous() * (r + 1)
+          for r in range(n)]  # shapes (1,2), (5,2), (9,2)
+    outs = repl.run(step, lambda r: xs[r])
+    for r in range(n):
+        g, mg, mr = outs[r]
+        assert [tuple(t.shape) for t in g] == [(1, 2), (5, 2), (9, 2)]
+        for q in range(n):
+            assert torch.equal(g[q], xs[q])
+        assert [host(t).tolist() for t in mg.value] == [host(x.sum(0)).tolist() for x in xs]
+        assert float(host(mr.value)) == float(sum(host(x).sum() for x in xs))
+    with pytest.raises(errors.ProtocolError):  # trailing dimensions must agree
+        repl.run(lambda x: repl.all_gather(x, ragged=True),
+                 lambda r: torch.zeros((2, 2 + (r == 1)), device=DEV))
+    repl.comm.close()
