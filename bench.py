@@ -13,7 +13,7 @@ cooperative launch (replica = blockIdx.y): HBM-bound. At N>1 each GPU is one rep
 and the kernel's loads/stores cross NVLink: NVLink-bound.
 
 value = n_gpus x busBW (nccl-tests busBW = 2(R-1)/R * S / t, per GPU), i.e. the
-aggregate bus bandwidth of the job. L2 is flushed (256 MiB write) between timed
+aggregate bus bandwidth of the job. L2 is flushed (256 MiB write + 256 MiB read) between timed
 steps; every step is timed with CUDA events around the one collective launch; the
 max over ranks is reported.
 """
@@ -53,6 +53,10 @@ def parse():
                         "in-switch reduction beats the P2P two-shot; the library then picks it under --algo auto)")
     p.add_argument("--ar-impl", default=None, choices=["push", "pull"],
                    help="force the all-reduce data-movement form (default: push multi-process, pull virtual)")
+    p.add_argument("--flush", default="write+read", choices=["write", "write+read"],
+                   help="L2 flush before every timed step: write 256 MiB (leaves up to the L2's worth of dirty "
+                        "lines to be written back INSIDE the timed step), or write 256 MiB then read another "
+                        "256 MiB (the flush's write-backs complete before the step; L2 clean and cold)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=10.0)
     p.add_argument("--e2e-steps", type=int, default=10)
@@ -188,7 +192,9 @@ def _config(args, world):
                                                       else f" on {world} B200 (one per process, NVLink P2P)")),
             "msg_bytes_per_replica": args.bytes, "replicas": n, "dtype": "f32", "op": args.kind,
             "algo": getattr(args, "chosen_algo", args.algo), "algo_requested": args.algo,
-            "in_place_pool": True, "l2": "flushed between steps (256 MiB write)",
+            "in_place_pool": True, "l2": ("flushed between steps (256 MiB write + 256 MiB read: clean, cold L2)"
+                                          if getattr(args, "flush", "write") == "write+read"
+                                          else "flushed between steps (256 MiB write)"),
             "parallelism": f"dp{n}"}
 
 
@@ -238,6 +244,7 @@ def run_ours(args, rank, world, local):
         def align():
             comm.all_reduce_tensor(tiny, "sum", out=tiny)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.zeros(64 << 20, dtype=torch.float32, device=dev) if args.flush == "write+read" else None
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -257,6 +264,8 @@ def run_ours(args, rank, world, local):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.zero_()
+        if flush_rd is not None:
+            flush_rd.sum()  # evicts the flush's dirty lines now, not inside the timed step
         if align is not None:
             align()  # untimed tiny collective: ranks leave the flush together (no skew in the step)
         evs[i][0].record(stream)
