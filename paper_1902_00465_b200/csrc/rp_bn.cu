@@ -95,13 +95,10 @@ __device__ __forceinline__ void load_nv(const T* p, double (&out)[NV]) {
 // per thread), accumulation is f64, and the RY row-partials of a channel are
 // folded in a fixed order through shared memory.
 template <typename T, bool BWD, int NV>
-__global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
-  // raw 16-byte packets stay in registers until accumulated (4 regs per packet),
-  // so 8 rows per thread can be in flight without spilling
+__device__ __forceinline__ void nhwc_partial(const BnArgs& a, int rep, double* smem) {
+  // raw 16-byte packets stay in registers until accumulated (4 regs per packet)
   constexpr bool kPacked = NV * sizeof(T) == 16;
-  constexpr int U = kPacked ? (BWD ? 4 : 8) : 4;
-  extern __shared__ double smem[];
-  const int rep = blockIdx.z;
+  constexpr int U = kPacked ? (BWD ? 2 : 4) : 4;  // packed: x2 with the prefetch buffer
   const T* x = (const T*)a.x[rep];
   const T* dy = BWD ? (const T*)a.dy[rep] : nullptr;
   const int64_t C = a.C, M = a.rows;
@@ -123,17 +120,27 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
     mu[k] = BWD ? (double)a.mean[rep][c0 + k] : 0.0;
   }
   if (active && kPacked) {
+    // software pipeline: the next U rows are requested before the current U are
+    // accumulated, so every warp always has U x 16 B in flight (single-buffered,
+    // a warp stopped loading while it accumulated in f64: ~half the bytes in
+    // flight, 53% of HBM, ncu profiles/r01_ncu_bn.txt)
     const int64_t step = (int64_t)RY * U;
-    for (int64_t r = r0 + ry; r < r1; r += step) {
-      uint4 px[U], pd[U];
+    uint4 px[U], pd[U];
+    auto load = [&](int64_t r, uint4 (&bx)[U], uint4 (&bd)[U]) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t rr = r + (int64_t)u * RY;
         if (rr < r1) {
-          px[u] = ld128_stream(x + rr * C + c0);
-          if (BWD) pd[u] = ld128_stream(dy + rr * C + c0);
+          bx[u] = ld128_stream(x + rr * C + c0);
+          if (BWD) bd[u] = ld128_stream(dy + rr * C + c0);
         }
       }
+    };
+    int64_t r = r0 + ry;
+    if (r < r1) load(r, px, pd);
+    for (; r < r1; r += step) {
+      uint4 nx[U], nd[U];
+      if (r + step < r1) load(r + step, nx, nd);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (r + (int64_t)u * RY < r1) {
@@ -153,6 +160,11 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
             }
           }
         }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        px[u] = nx[u];
+        if (BWD) pd[u] = nd[u];
       }
     }
   } else if (active) {
@@ -207,6 +219,12 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
       P[(c0 + k) * 2 + 1] = s2[k];
     }
   }
+}
+
+template <typename T, bool BWD, int NV>
+__global__ void __launch_bounds__(kBnThreads) bn_partial_nhwc(const BnArgs a) {
+  extern __shared__ double smem[];
+  nhwc_partial<T, BWD, NV>(a, blockIdx.z, smem);
 }
 
 // --- NCHW: x is [n, C, hw] ---------------------------------------------------
@@ -293,13 +311,12 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nchw(const BnArgs a) {
 // partial sums are then folded in lane order through shared memory -- a
 // deterministic order, parallel over the S split partials (a serial loop over S at
 // L2 latency dominated small layers).
-__global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
+__device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk) {
   __shared__ double red[kExThreads][2];
-  const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
   const int rep = a.rank >= 0 ? 0 : rank;  // local replica index
   const int tpc = kExThreads / a.cpb;      // threads per channel
   const int lane = threadIdx.x % tpc;
-  const int64_t c = (int64_t)blockIdx.x * a.cpb + threadIdx.x / tpc;
+  const int64_t c = (int64_t)blk * a.cpb + threadIdx.x / tpc;
   const int64_t C = a.C;
   {
     double s1 = 0.0, s2 = 0.0;
@@ -330,9 +347,9 @@ __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
     rec[1] = s2;
     rec[2] = a.local_count[rep];
   }
-  const int es = RP_ST_BN_EPOCH + blockIdx.x;
+  const int es = RP_ST_BN_EPOCH + blk;
   const uint32_t e0 = epoch_begin(a.t, rank, es);
-  if (!rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, e0 + 1)) return;
+  if (!rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blk, e0 + 1)) return;
   if (lane == 0 && c < C) {
     double A1 = 0.0, A2 = 0.0, Mt = 0.0;
     for (int p = 0; p < a.world; ++p) {  // ascending rank order
@@ -354,8 +371,52 @@ __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
     }
     if (c == 0 && a.count[rep]) *a.count[rep] = Mt;
   }
-  rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blockIdx.x, e0 + 2);
+  rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blk, e0 + 2);
   epoch_end(a.t, rank, es, e0 + 2);
+}
+
+__global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
+  exchange_body(a, a.rank >= 0 ? a.rank : (int)blockIdx.y, blockIdx.x);
+}
+
+// --- fused statistics (NHWC): the local pass and the cross-replica reduction in
+// ONE cooperative launch (one wave of co-resident blocks per replica):
+//   every block: its split's per-channel partials (nhwc_partial)
+//   device-wide barrier (monotone counter; the consumed base lives in the local
+//     sequencing state, so graph replays stay in step)
+//   blocks 0..ex_blocks-1: fold the split partials of their channels (fixed
+//     order), publish, meet the peers on their BN row, fold ranks in ascending
+//     order, write the outputs (exchange_body)
+// Saves the second launch and lets up to 256 blocks fold the partials.
+struct FusedBnArgs {
+  BnArgs b;
+  ExArgs e;
+  int ex_blocks;
+};
+
+template <typename T, bool BWD, int NV>
+__global__ void __launch_bounds__(kBnThreads) bn_stats_fused(const FusedBnArgs f) {
+  extern __shared__ double smem[];
+  const int rank = f.e.rank >= 0 ? f.e.rank : (int)blockIdx.z;
+  const int rep = f.e.rank >= 0 ? 0 : rank;
+  const uint32_t total = gridDim.x * gridDim.y;
+  const uint32_t bid = blockIdx.y * gridDim.x + blockIdx.x;
+  const uint32_t base = state_load(f.e.t, rank, RP_ST_BN_GRID_BASE);
+  nhwc_partial<T, BWD, NV>(f.b, rep, smem);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* ctr = f.e.t.sig[rank] + RP_ST_BN_GRID_CTR;
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while ((int32_t)(v - (base + total)) < 0);
+  }
+  __syncthreads();
+  if ((int)bid >= f.ex_blocks) return;
+  exchange_body(f.e, rank, (int)bid);
+  if (bid == 0 && threadIdx.x == 0) state_store(f.e.t, rank, RP_ST_BN_GRID_BASE, base + total);
 }
 
 // --- elementwise apply ----------------------------------------------------------
@@ -483,6 +544,19 @@ const void* pick_partial(int dtype, int layout, bool vec) {
   return nullptr;
 }
 
+template <bool BWD>
+const void* pick_fused(int dtype, bool vec) {
+#define RP_F(DT, T)                                                                    \
+  if (dtype == DT)                                                                     \
+    return vec ? (const void*)bn_stats_fused<T, BWD, 16 / sizeof(T)> : (const void*)bn_stats_fused<T, BWD, 1>;
+  RP_F(RP_F32, float)
+  RP_F(RP_BF16, __nv_bfloat16)
+  RP_F(RP_F16, __half)
+  RP_F(RP_F64, double)
+#undef RP_F
+  return nullptr;
+}
+
 int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, int64_t rows, int64_t ch, int64_t hw,
               int layout, float eps, const float* mean, float* o0, float* o1, float* o2, float* o3, double* count,
               cudaStream_t stream) {
@@ -520,7 +594,16 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   }
   dim3 grid, block;
   size_t smem = 0;
-  const int target = 3 * c->num_sms;  // ~resident blocks: enough bytes in flight, few split partials
+  // one full wave of co-resident blocks: bytes in flight on every SM and no
+  // partial last wave (444 blocks at 2 resident per SM ran 1.5 waves, ncu)
+  int per_sm = 0;
+  {
+    const size_t smem0 = layout == RP_LAYOUT_NHWC ? (size_t)kBnThreads * 2 * nv * sizeof(double) : 0;
+    if (smem0 > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBnThreads, smem0) != cudaSuccess || per_sm < 1)
+      per_sm = 2;
+  }
+  const int target = per_sm * c->num_sms / nrep;
   if (layout == RP_LAYOUT_NHWC) {
     block = dim3(kBnThreads);
     const int64_t cvt = ch / nv;  // channel-vectors per row
@@ -538,6 +621,27 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
     a.S = S;
     grid = dim3((unsigned)ch, S, nrep);
   }
+  // Fused single launch (NHWC): the grid must be one co-resident wave per replica
+  // set and hold at least one block per exchange group (<= 256 BN rows); when it
+  // cannot (huge C with many virtual replicas) the two-kernel path runs instead.
+  bool fused = layout == RP_LAYOUT_NHWC && getenv("RP_BN_UNFUSED") == nullptr;
+  const void* ff = nullptr;
+  int fcpb = 1, fex = 0;
+  if (fused) {
+    ff = bwd ? pick_fused<true>(dtype, vecok) : pick_fused<false>(dtype, vecok);
+    if (smem > 48 * 1024)
+      RP_CUDA_CHECK(cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int fper = 0;
+    RP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fper, ff, kBnThreads, smem));
+    const int64_t wave = (int64_t)fper * c->num_sms / nrep;  // co-resident blocks per replica
+    if ((int64_t)grid.x * grid.y > wave) grid.y = (unsigned)std::max<int64_t>(1, wave / grid.x);
+    const int64_t emax = std::min<int64_t>(RP_BN_ROWS, wave);
+    while (fcpb < kExThreads && (ch + fcpb - 1) / fcpb > emax) fcpb *= 2;
+    fex = (int)((ch + fcpb - 1) / fcpb);
+    if ((int64_t)grid.x * grid.y < fex) grid.y = (unsigned)((fex + grid.x - 1) / grid.x);  // empty splits: zeros
+    fused = fex <= emax && (int64_t)grid.x * grid.y <= wave;
+    if (fused) a.S = (int)grid.y;
+  }
   const size_t per_rep = (size_t)a.S * ch * 2 * sizeof(double);
   int rc = ensure_partials(c, per_rep * nrep);
   if (rc) return rc;
@@ -545,10 +649,10 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   if (smem > 48 * 1024) {
     RP_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
-  if (rows > 0) {
+  if (!fused && rows > 0) {
     void* args[] = {&a};
     RP_CUDA_CHECK(cudaLaunchKernel(fn, grid, block, args, smem, stream));
-  } else {
+  } else if (!fused) {
     RP_CUDA_CHECK(cudaMemsetAsync(c->bn_partials, 0, per_rep * nrep, stream));
   }
 
@@ -579,6 +683,16 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
       e.out3[i] = o3;
       e.count[i] = count;
     }
+  }
+  if (fused) {  // one launch: partials, device-wide barrier, exchange (bn_stats_fused)
+    e.cpb = fcpb;
+    FusedBnArgs fa;
+    fa.b = a;
+    fa.e = e;
+    fa.ex_blocks = fex;
+    void* fargs[] = {&fa};
+    RP_CUDA_CHECK(cudaLaunchCooperativeKernel(ff, grid, block, fargs, smem, stream));
+    return RP_OK;
   }
   // exchange geometry: as many blocks as the BN signal rows and co-residency allow,
   // >= 16 channels per block, the rest of the 256 threads fold split partials

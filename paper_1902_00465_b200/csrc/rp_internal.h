@@ -30,11 +30,16 @@
 //   bn_epoch[b]   same for the BN exchange rows
 //   zone_par[b]   one-shot landing-zone parity of block b
 //   ph_seen[k]    arrivals already consumed per source rank on phase row k
+//   bn_grid       fused BN kernel's device-wide barrier (counter, consumed base)
 #define RP_STATE_WORD (12 * 1024)
 #define RP_ST_BLK_EPOCH (RP_STATE_WORD)
 #define RP_ST_BN_EPOCH (RP_ST_BLK_EPOCH + RP_MAX_BLOCKS)
 #define RP_ST_ZONE_PAR (RP_ST_BN_EPOCH + 256)
 #define RP_ST_PH_SEEN (RP_ST_ZONE_PAR + RP_MAX_BLOCKS)
+// fused BN statistics kernel: device-wide barrier (monotone arrival counter and
+// the count already consumed by earlier calls)
+#define RP_ST_BN_GRID_CTR (RP_ST_PH_SEEN + 8)
+#define RP_ST_BN_GRID_BASE (RP_ST_PH_SEEN + 9)
 #define RP_SIGNAL_BYTES (64 * 1024)  // signal region ahead of the data
 #define RP_ALIGN 256
 // Pool layout (every rank identical):

@@ -34,6 +34,7 @@ def main():
     p.add_argument("--iters", type=int, default=20)
     p.add_argument("--dtype", default="f32")
     p.add_argument("--out", default=None)
+    p.add_argument("--only", default=None, help="one shape, e.g. 256x64 (C x H)")
     a = p.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -54,7 +55,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     rows_out = []
-    for (c, h) in SHAPES:
+    shapes = SHAPES if a.only is None else [tuple(int(v) for v in a.only.split("x"))]
+    for (c, h) in shapes:
         n = a.batch
         xs = [torch.randn(n, c, h, h, device=dev).to(dt).contiguous(memory_format=torch.channels_last)
               for _ in range(nrep)]
