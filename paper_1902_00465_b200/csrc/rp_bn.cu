@@ -99,6 +99,7 @@ __device__ __forceinline__ void nhwc_partial(const BnArgs& a, int rep, double* s
   // raw 16-byte packets stay in registers until accumulated (4 regs per packet)
   constexpr bool kPacked = NV * sizeof(T) == 16;
   // packed: x2 with the prefetch buffer; f32 forward is latency-bound at 4 rows
+  // (16-bit types: 8/4 rows need 150-160 registers, 1 block per SM: slower, measured)
   constexpr int U = kPacked ? (sizeof(T) == 4 ? (BWD ? 4 : 8) : (BWD ? 2 : 4)) : 4;
   const T* x = (const T*)a.x[rep];
   const T* dy = BWD ? (const T*)a.dy[rep] : nullptr;
