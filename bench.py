@@ -130,6 +130,20 @@ def peaks():
         return HBM_FALLBACK_GBS, "fallback"
 
 
+def ncu_traffic(key: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/r01_ncu_traffic.json), or (None, None) when none matches."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f).get(key)
+    except (OSError, ValueError):
+        return None, None
+    if not rec:
+        return None, None
+    return rec["dram_read_bytes"] + rec["dram_write_bytes"], rec["source"]
+
+
 def busbw(nbytes, n, seconds):
     return 2.0 * (n - 1) / n * nbytes / seconds / 1e9
 
@@ -284,9 +298,13 @@ def run_ours(args, rank, world, local):
     if world == 1:
         alg_bytes = 2.0 * n * args.bytes  # every replica buffer read once, written once
         achieved = alg_bytes / (ms / 1e3) / 1e9
+        kname = f"ar_twoshot<f32,premean,{n}>"
+        traffic, tsrc = ncu_traffic(f"{kname}@{args.bytes}")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
-                    "algorithmic_bytes_per_launch": alg_bytes, "kernel": "ar_twoshot<f32,premean,8>"}
+                    "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
+                    "algorithmic_bytes_per_launch": alg_bytes, "kernel": kname}
+        if tsrc:
+            roofline["traffic_source"] = tsrc
     else:
         # busBW = 2(N-1)/N * S / t against the per-direction link peak (the nccl-tests
         # convention); the bytes one GPU's links actually carry per direction are

@@ -66,24 +66,28 @@ class _Bucket:
             out.append(g)
         return out
 
-    def pack(self):
+    def pack(self, grads=None):
         """Every replica's gradients -> its flat bucket (one multi-tensor launch each,
-        with the exchange cast fused). Returns the gradient lists (for unpack)."""
+        with the exchange cast fused). Returns the gradient lists (for unpack).
+        ``grads``: the lists from ``_grads`` when the caller fetched them already
+        (overlap.py fetches them on the compute stream, packs on the comm stream)."""
         lib = _lib.load()
         stream = torch.cuda.current_stream(self.flat[0].device).cuda_stream
         gcode, ccode = dtype_code(self.grad_dtype), dtype_code(self.comm_dtype)
-        grads = [self._grads(r) for r in range(len(self.params))]
+        if grads is None:
+            grads = [self._grads(r) for r in range(len(self.params))]
         for r, flat in enumerate(self.flat):
             pp, k = _lib.ptr_array([g.data_ptr() for g in grads[r]])
             _lib.check(lib.rp_pack(flat.data_ptr(), ccode, pp, self._counts_c[0], self._offs_c[0], len(grads[r]),
                                    gcode, stream), "pack")
         return grads
 
-    def reduce(self, kind: str):
+    def reduce(self, kind: str, grads=None):
+        """pack -> in-place premean/sum fold -> unpack, all on the current stream."""
         lib = _lib.load()
         stream = torch.cuda.current_stream(self.flat[0].device).cuda_stream
         gcode, ccode = dtype_code(self.grad_dtype), dtype_code(self.comm_dtype)
-        grads = self.pack()
+        grads = self.pack(grads)
         keep = []
         if isinstance(self.comm, VirtualCommunicator):
             self.comm.all_reduce(self.flat, kind, outs=self.flat)

@@ -279,9 +279,13 @@ class Replicator:
                     if self.comm.world > 1:
                         self.comm.broadcast_tensor(tensors[0][k].data, root=0)
 
-    def wrap_optimizer(self, optimizer, kind: str = "premean", fused: bool = False):
+    def wrap_optimizer(self, optimizer, kind: str = "premean", fused: bool = False, overlap: bool = False):
         """apply_gradients first averages every gradient across
         replicas with all_sum(g / R), then applies the base rule.
+
+        ``overlap=True`` (one replica per process): the same averaging, started
+        bucket by bucket from post-accumulate-grad hooks on a side stream while
+        backward runs (overlap.py); ``step()`` joins it.
 
         ``fused=True`` (torch.optim.SGD / Adam / AdamW, f32 parameters): the
         average and the update run as one kernel that updates each rank's shard and
@@ -296,8 +300,13 @@ class Replicator:
         if fused:
             if kind != "premean":
                 raise errors.ConfigurationError("fused apply averages with the premean fold")
+            if overlap:
+                raise errors.ConfigurationError("fused=True and overlap=True are exclusive")
             from .fused import FusedReplicatedOptimizer
             return FusedReplicatedOptimizer(self, opts)
+        if overlap:
+            from .overlap import OverlappedReplicatedOptimizer
+            return OverlappedReplicatedOptimizer(self, opts[0], kind)
         return ReplicatedOptimizer(self, opts, kind)
 
     # -- run ----------------------------------------------------------------

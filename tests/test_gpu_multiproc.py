@@ -556,6 +556,72 @@ def body_timeout(rank, world):
     comm.close()
 
 
+def body_overlap(rank, world):
+    """wrap_optimizer(overlap=True): buckets exchanged from post-accumulate-grad
+    hooks on a side stream during backward must give the SAME bits as the
+    synchronous wrapped optimizer (same premean fold per element), including with
+    a bf16 exchange, unused parameters and no_sync() gradient accumulation."""
+    from paper_1902_00465_b200 import errors
+    from paper_1902_00465_b200.replicator import Replicator
+
+    dev = torch.device(f"cuda:{rank}")
+
+    def net():
+        return torch.nn.Sequential(torch.nn.Conv2d(3, 16, 3, padding=1), torch.nn.ReLU(),
+                                   torch.nn.Conv2d(16, 32, 3, padding=1), torch.nn.ReLU(),
+                                   torch.nn.AdaptiveAvgPool2d(1), torch.nn.Flatten(), torch.nn.Linear(32, 10))
+
+    for comm_dt in (None, torch.bfloat16):
+        results = []
+        for overlap in (False, True):
+            repl = Replicator(device=rank, pool_bytes=32 << 20, grad_comm_dtype=comm_dt,
+                              bucket_bytes=(2 << 10) if overlap else None)
+            torch.manual_seed(rank)
+            with repl.context():
+                model = repl.replicate(lambda: net().to(memory_format=torch.channels_last))
+                unused = repl.replicate(lambda: torch.nn.Linear(4, 4))  # never receives a gradient
+                params = list(unused.local.parameters()) + list(model.local.parameters())  # unused -> last bucket
+                opt = repl.wrap_optimizer(torch.optim.SGD(params, lr=0.05, momentum=0.9), overlap=overlap)
+            if overlap:
+                assert len(opt.buckets) > 3, "small bucket_bytes must give several buckets"
+            for step in range(4):
+                g = torch.Generator().manual_seed(10 * step + rank)
+                opt.zero_grad(set_to_none=(step % 2 == 1))
+                micro = 2 if step == 3 else 1
+                for m in range(micro):
+                    xb = torch.randn(8, 3, 12, 12, generator=g).to(dev).contiguous(memory_format=torch.channels_last)
+                    yb = torch.randint(0, 10, (8,), generator=g).to(dev)
+                    ctx = opt.no_sync() if (overlap and m < micro - 1) else _nullcontext()
+                    with ctx:
+                        torch.nn.functional.cross_entropy(model.local(xb), yb).backward()
+                opt.step()
+            torch.cuda.synchronize()
+            results.append([p.detach().clone() for p in params])
+            if overlap:  # accumulating twice without no_sync is refused
+                opt.zero_grad()
+                xb = torch.randn(8, 3, 12, 12, device=dev).contiguous(memory_format=torch.channels_last)
+                torch.nn.functional.cross_entropy(model.local(xb), torch.zeros(8, dtype=torch.long, device=dev)) \
+                    .backward()
+                with pytest.raises(Exception) as ei:
+                    torch.nn.functional.cross_entropy(model.local(xb), torch.zeros(8, dtype=torch.long,
+                                                                                   device=dev)).backward()
+                assert "no_sync" in str(ei.value) or isinstance(ei.value, errors.ProtocolError)
+                opt.remove_hooks()
+            repl.comm.close()
+        for a, b in zip(*results):
+            assert torch.equal(a, b), f"overlap differs from the synchronous wrapped optimizer ({comm_dt})"
+        flat = torch.cat([p.reshape(-1) for p in results[1]])
+        import torch.distributed as dist
+        gl = [torch.empty_like(flat.cpu()) for _ in range(world)]
+        dist.all_gather(gl, flat.cpu())
+        assert all(torch.equal(t, gl[0]) for t in gl), "replicas diverged"
+
+
+def _nullcontext():
+    import contextlib
+    return contextlib.nullcontext()
+
+
 # ---------------------------------------------------------------------------
 
 def test_all_reduce_multiprocess():
@@ -600,3 +666,7 @@ def test_cuda_graph_replay_multiprocess():
 
 def test_dead_rank_times_out():
     run_world("body_timeout")
+
+
+def test_overlapped_wrap_optimizer_multiprocess():
+    run_world("body_overlap")

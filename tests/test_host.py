@@ -187,3 +187,29 @@ def test_bootstrap_exchange_world2_gloo():
     for p in ps:
         p.join(timeout=30)
     assert res == {0: True, 1: True}
+
+
+def test_overlap_launcher_keeps_bucket_order():
+    """overlap.py: buckets that become ready out of order are held until their
+    predecessors launched, so every rank issues the same collective sequence."""
+    from paper_1902_00465_b200.overlap import InOrderLauncher
+    lo = InOrderLauncher(4)
+    assert lo.mark(2) == []
+    assert lo.mark(0) == [0]
+    assert lo.mark(1) == [1, 2]
+    with pytest.raises(errors.ProtocolError):
+        lo.mark(1)
+    assert lo.rest() == [3]
+    lo.reset()
+    assert lo.mark(0) == [0] and lo.rest() == [1, 2, 3]
+
+
+def test_overlap_bucket_plan_reverse_order_per_dtype():
+    from paper_1902_00465_b200.overlap import bucket_plan
+    sizes = [100, 50, 50, 200, 30, 30]
+    dts = ["f", "f", "h", "f", "f", "h"]
+    plan = bucket_plan(sizes, dts, limit=100)
+    # reverse order; a dtype change does not close the other dtype's bucket;
+    # an oversize gradient gets a bucket of its own
+    assert plan == [[5, 2], [4], [3], [1], [0]]
+    assert sorted(i for b in plan for i in b) == list(range(6))

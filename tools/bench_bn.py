@@ -35,6 +35,9 @@ def main():
     p.add_argument("--dtype", default="f32")
     p.add_argument("--out", default=None)
     p.add_argument("--only", default=None, help="one shape, e.g. 256x64 (C x H)")
+    p.add_argument("--flush", default="write+read", choices=["write", "write+read"],
+                   help="L2 flush between iterations; write+read leaves clean lines, so the flush's "
+                        "dirty-line drain does not land inside the timed kernel")
     a = p.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -53,6 +56,7 @@ def main():
     code = {"f32": 0, "bf16": 2}[a.dtype]
     lib = _lib.load()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_sink = torch.empty((), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
     rows_out = []
     shapes = SHAPES if a.only is None else [tuple(int(v) for v in a.only.split("x"))]
@@ -103,6 +107,8 @@ def main():
                 torch.distributed.barrier()
             for e0, e1 in evs:
                 flush.zero_()
+                if a.flush == "write+read":
+                    flush_sink.copy_(flush.view(torch.int64).sum())
                 e0.record(stream)
                 fn()
                 e1.record(stream)

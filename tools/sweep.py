@@ -73,6 +73,8 @@ def main():
     for op in a.ops.split(","):
         algos = a.algos.split(",") if op == "all_reduce" else (["auto", "direct", "scatter"] if op == "broadcast"
                                                                 else ["auto"])
+        if "nccl" in a.algos.split(",") and op != "all_reduce":
+            algos = algos + ["nccl"]  # comparison column only: NCCL is never on the product path
         for lg in range(a.min_log2, a.max_log2 + 1):
             size = 1 << lg
             count = size // 4
@@ -84,6 +86,10 @@ def main():
                     os_ = [o[:count] for o in outs]
                     if world == 1:
                         fn = lambda: comm.all_reduce(xs, "sum", outs=os_, algo=algo)  # noqa: E731
+                    elif algo == "nccl":
+                        if world == 1:
+                            continue
+                        fn = lambda: torch.distributed.all_reduce(os_[0])  # noqa: E731
                     elif algo == "nvls":
                         if nvls_buf is None:
                             continue
@@ -94,14 +100,22 @@ def main():
                     factor = 2.0 * (n - 1) / n
                 elif op == "all_gather":
                     os_ = [o[:n * count].view(n, count) for o in outs]
-                    if world == 1:
+                    if algo == "nccl":
+                        if world == 1:
+                            continue
+                        fn = lambda: torch.distributed.all_gather_into_tensor(os_[0].view(-1), xs[0])  # noqa: E731
+                    elif world == 1:
                         fn = lambda: comm.all_gather(xs, outs=os_)  # noqa: E731
                     else:
                         fn = lambda: comm.all_gather_tensor(xs[0], out=os_[0])  # noqa: E731
                     factor = float(n - 1)
                 else:
                     os_ = [o[:count] for o in outs]
-                    if world == 1:
+                    if algo == "nccl":
+                        if world == 1:
+                            continue
+                        fn = lambda: torch.distributed.broadcast(os_[0], src=0)  # noqa: E731
+                    elif world == 1:
                         fn = lambda: comm.broadcast(xs, root=0, outs=os_, algo=algo)  # noqa: E731
                     else:
                         fn = lambda: comm.broadcast_tensor(xs[0], root=0, out=os_[0], algo=algo)  # noqa: E731

@@ -40,6 +40,9 @@ def main():
                    help="wrap_optimizer(fused=True): average + SGD update of each rank's shard in one kernel")
     p.add_argument("--nvls", action="store_true",
                    help="place the gradient buckets in an NVSwitch multicast region (in-switch reduction at >= 4)")
+    p.add_argument("--overlap", action="store_true",
+                   help="wrap_optimizer(overlap=True): buckets exchanged from grad hooks during backward")
+    p.add_argument("--bucket-mb", type=float, default=None, help="fusion bucket size (overlap)")
     a = p.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -57,12 +60,14 @@ def main():
     torch.backends.cudnn.allow_tf32 = True
     repl = Replicator(device=local, pool_bytes=512 << 20,
                       grad_comm_dtype=torch.bfloat16 if a.grad_comm == "bf16" else None,
-                      nvls_bytes=(128 << 20) if (a.nvls and world > 1) else 0)
+                      nvls_bytes=(128 << 20) if (a.nvls and world > 1) else 0,
+                      bucket_bytes=int(a.bucket_mb * (1 << 20)) if a.bucket_mb else None)
     torch.manual_seed(rank)  # replicate() broadcasts replica 0's init
     with repl.context():
         model = repl.replicate(lambda: torchvision.models.resnet50().to(memory_format=torch.channels_last))
         opt = repl.wrap_optimizer(torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, nesterov=True,
-                                                  weight_decay=1e-4), fused=a.fused)
+                                                  weight_decay=1e-4), fused=a.fused,
+                                   overlap=a.overlap and world > 1)
     net = model.local
     if a.no_average:
         opt.average_gradients = lambda: None
@@ -130,6 +135,8 @@ def main():
         for _ in range(10):
             if a.fused:  # pack + fused average/update (the whole optimizer step)
                 opt._apply_all()
+            elif a.overlap and world > 1:  # every bucket, as step() launches them without backward
+                opt.average_gradients()
             else:
                 opt._buckets.reduce("premean")
         a1.record(stream)
@@ -146,6 +153,8 @@ def main():
     if rank == 0:
         if a.fused:
             grad_bytes = sum(g.grads.numel * g.grads.flat[0].element_size() for g in opt.groups if g is not None)
+        elif a.overlap and world > 1:
+            grad_bytes = sum(b.numel * b.flat[0].element_size() for b in opt.buckets)
         else:
             grad_bytes = sum(b.numel * b.flat[0].element_size() for b in opt._buckets.buckets) if opt._buckets else 0
         line = {"metric": "ResNet-50 synthetic img/s", "value": world * a.batch / (ms / 1e3), "unit": "img/s",
@@ -153,6 +162,7 @@ def main():
                 "allreduce_ms": ar_ms, "allreduce_share": ar_ms / ms if ms else 0.0,
                 "grad_exchange_bytes": grad_bytes, "grad_comm": a.grad_comm, "replicas_identical": consistent,
                 "loss": float(loss.item()), "wall_s": wall, "fused_apply": a.fused, "nvls": a.nvls,
+                "overlap": a.overlap, "buckets": len(opt.buckets) if (a.overlap and world > 1) else None,
                 "config": {"model": "resnet50 (torchvision, random init)", "input": "synthetic 224x224x3 channels_last",
                            "precision": "bf16 autocast, fp32 master", "optimizer": "SGD nesterov 0.9 wd 1e-4"}}
         print(json.dumps(line), flush=True)
