@@ -127,6 +127,15 @@ RP_API int rp_comm_check(rp_comm_t comm);
 /* Spin timeout for cross-rank waits, nanoseconds (default 20 s). */
 RP_API int rp_comm_set_timeout(rp_comm_t comm, uint64_t ns);
 
+/* Cap the grid of every later collective launch at `blocks` blocks per rank (0 =
+ * no cap: as many co-resident blocks as the kernel allows). Used while a
+ * collective runs beside compute kernels (wrap_optimizer overlap: the exchange
+ * leaves the other SMs to backward). Kernels whose blocks pair up by index across
+ * ranks rely on equal grids: set it identically on every rank, at the same point
+ * of the collective sequence. No reference counterpart (the reference's
+ * collectives run after the whole backward). */
+RP_API int rp_comm_set_block_cap(rp_comm_t comm, int blocks);
+
 /* ---- NVLS (NVLink SHARP) region ------------------------------------------ */
 /* A multicast object spanning all ranks' GPUs with `bytes` of each rank's memory
  * bound to it (RP_ALGO_NVLS reduces inside the NVSwitch). Bootstrap order, every

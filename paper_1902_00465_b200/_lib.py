@@ -63,6 +63,7 @@ SIGNATURES = {
     "rp_comm_reserve": (_i, [_c_void_p, _size_t]),
     "rp_comm_check": (_i, [_c_void_p]),
     "rp_comm_set_timeout": (_i, [_c_void_p, ctypes.c_uint64]),
+    "rp_comm_set_block_cap": (_i, [_c_void_p, ctypes.c_int]),
     "rp_all_reduce": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _i, _i, _i, _c_void_p]),
     "rp_all_gather": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _c_void_p]),
     "rp_broadcast": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _c_void_p]),

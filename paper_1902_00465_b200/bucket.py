@@ -25,8 +25,18 @@ _ALIGN_ELEMS = 64  # keep every tensor's slot 128-byte aligned for 16-bit types
 
 
 class _Bucket:
+    """``views=True`` (gradients as bucket views): the bucket holds the gradients
+    themselves in their own dtype, and every ``param.grad`` is a view of its slot
+    (same strides as the parameter). Autograd accumulates in place into the pool,
+    so the exchange needs no pack and no unpack: ONE in-place all-reduce per bucket,
+    with the exchange cast (e.g. f32 gradients sent as bf16) fused into the kernel.
+    The arithmetic is the same as pack (RNE cast) -> fold -> unpack (exact widening),
+    so results are bit-identical to the packed form. A gradient that stopped being
+    a view (``zero_grad(set_to_none=True)``, a user assignment) is copied back into
+    its slot and re-attached before the exchange."""
+
     def __init__(self, comm, params_per_replica, grad_dtype, comm_dtype, allow_nvls: bool = True,
-                 match_param_layout: bool = False):
+                 match_param_layout: bool = False, views: bool = False):
         self.comm = comm
         self.grad_dtype = grad_dtype
         self.comm_dtype = comm_dtype
@@ -38,15 +48,60 @@ class _Bucket:
             o += (n + _ALIGN_ELEMS - 1) // _ALIGN_ELEMS * _ALIGN_ELEMS
         self.offs = offs
         self.numel = o
-        esz = torch.empty((), dtype=comm_dtype).element_size()
+        self.views = bool(views) and all(_is_dense(p) for p in params_per_replica[0])
+        flat_dtype = grad_dtype if self.views else comm_dtype
+        esz = torch.empty((), dtype=flat_dtype).element_size()
         self.match_param_layout = match_param_layout
-        if allow_nvls and isinstance(comm, Communicator) and comm.nvls_free >= o * esz + 256:
-            buf = comm.alloc_nvls(o, comm_dtype)  # reduced inside the NVSwitch (rp.h RP_ALGO_NVLS)
+        # the switch reduces in place without a cast (rp.h RP_ALGO_NVLS)
+        nvls_ok = flat_dtype == comm_dtype
+        if allow_nvls and nvls_ok and isinstance(comm, Communicator) and comm.nvls_free >= o * esz + 256:
+            buf = comm.alloc_nvls(o, flat_dtype)  # reduced inside the NVSwitch
         else:
-            buf = comm.alloc(o, comm_dtype)
+            buf = comm.alloc(o, flat_dtype)
         self.flat = buf if isinstance(buf, list) else [buf]
         self._counts_c = _lib.i64_array(self.counts)
         self._offs_c = _lib.i64_array(self.offs)
+        if self.views:
+            self.slots = [[flat[off:off + n].as_strided(p.shape, p.stride())
+                           for p, off, n in zip(self.params[r], self.offs, self.counts)]
+                          for r, flat in enumerate(self.flat)]
+            for flat in self.flat:
+                flat.zero_()
+            with torch.no_grad():
+                self.attach()
+
+    def attach(self):
+        """(views) Make every ``param.grad`` the view of its bucket slot, copying a
+        detached gradient back in (a missing one is zero). Returns the number of
+        gradients that had to be re-attached (0 in the steady state)."""
+        moved = 0
+        stream = torch.cuda.current_stream(self.flat[0].device)
+        for r, plist in enumerate(self.params):
+            same, ks = [], []  # same-layout gradients: one multi-tensor copy (K6 pack) into their slots
+            for k, (p, v) in enumerate(zip(plist, self.slots[r])):
+                g = p.grad
+                if g is not None and g.data_ptr() == v.data_ptr() and g.stride() == v.stride():
+                    continue
+                if g is None:
+                    v.zero_()
+                elif g.dtype == v.dtype and g.stride() == v.stride() and _is_dense(g):
+                    same.append(g)
+                    ks.append(k)
+                else:
+                    v.copy_(g)
+                if g is not None:
+                    g.record_stream(stream)
+                p.grad = v
+                moved += 1
+            if same:
+                lib = _lib.load()
+                code = dtype_code(self.grad_dtype)
+                pp, _keep = _lib.ptr_array([g.data_ptr() for g in same])
+                cnt, _k1 = _lib.i64_array([self.counts[k] for k in ks])
+                off, _k2 = _lib.i64_array([self.offs[k] for k in ks])
+                _lib.check(lib.rp_pack(self.flat[r].data_ptr(), code, pp, cnt, off, len(same), code,
+                                       stream.cuda_stream), "pack(attach)")
+        return moved
 
     def _grads(self, r):
         """The replica's gradients as dense storages. Pack/unpack copy storage order,
@@ -83,7 +138,17 @@ class _Bucket:
         return grads
 
     def reduce(self, kind: str, grads=None):
-        """pack -> in-place premean/sum fold -> unpack, all on the current stream."""
+        """pack -> in-place premean/sum fold -> unpack, all on the current stream
+        (views: attach, then the in-place fold with the cast fused)."""
+        if self.views:
+            with torch.no_grad():
+                self.attach()
+            cdt = None if self.comm_dtype == self.grad_dtype else self.comm_dtype
+            if isinstance(self.comm, VirtualCommunicator):
+                self.comm.all_reduce(self.flat, kind, outs=self.flat, comm_dtype=cdt)
+            else:
+                self.comm.all_reduce_tensor(self.flat[0], kind, out=self.flat[0], comm_dtype=cdt)
+            return
         lib = _lib.load()
         stream = torch.cuda.current_stream(self.flat[0].device).cuda_stream
         gcode, ccode = dtype_code(self.grad_dtype), dtype_code(self.comm_dtype)
@@ -108,7 +173,7 @@ class GradBuckets:
     """
 
     def __init__(self, comm, params_per_replica, comm_dtype: torch.dtype | None = None,
-                 bucket_bytes: int | None = None):
+                 bucket_bytes: int | None = None, views: bool = False):
         if isinstance(comm, Communicator) and len(params_per_replica) != 1:
             raise errors.ShapeError("a multi-process communicator reduces one replica per process")
         if isinstance(comm, VirtualCommunicator) and len(params_per_replica) != comm.world:
@@ -131,12 +196,13 @@ class GradBuckets:
             for i in idx:
                 nb = base[i].numel() * esz
                 if cur and cur_bytes + nb > limit:
-                    self.buckets.append(_Bucket(comm, [[lst[j] for j in cur] for lst in lists], dt, cdt))
+                    self.buckets.append(_Bucket(comm, [[lst[j] for j in cur] for lst in lists], dt, cdt,
+                                                views=views))
                     cur, cur_bytes = [], 0
                 cur.append(i)
                 cur_bytes += nb
             if cur:
-                self.buckets.append(_Bucket(comm, [[lst[j] for j in cur] for lst in lists], dt, cdt))
+                self.buckets.append(_Bucket(comm, [[lst[j] for j in cur] for lst in lists], dt, cdt, views=views))
 
     @property
     def nbytes(self) -> int:

@@ -125,6 +125,11 @@ class _Base:
     def set_timeout(self, seconds: float):
         _lib.check(self._lib.rp_comm_set_timeout(self._handle, int(seconds * 1e9)), "set_timeout")
 
+    def set_block_cap(self, blocks: int):
+        """At most ``blocks`` blocks per rank for later collective launches (0: no
+        cap). Set identically on every rank (include/rp.h rp_comm_set_block_cap)."""
+        _lib.check(self._lib.rp_comm_set_block_cap(self._handle, int(blocks)), "set_block_cap")
+
     # -- label protocol (SPEC.md:182-186, :236) -----------------------------
     def new_generation(self):
         """Start a new generation (training step): labels may be reused again."""

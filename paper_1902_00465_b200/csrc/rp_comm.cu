@@ -54,6 +54,7 @@ int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want) {
   int cap = occ * c->num_sms;
   if (c->is_virtual) cap /= c->world;
   cap = std::min(cap, RP_MAX_BLOCKS);
+  if (c->block_cap > 0) cap = std::min(cap, c->block_cap);
   return std::max(1, std::min(want, cap));
 }
 
@@ -387,6 +388,13 @@ int rp_comm_reserve(rp_comm_t c, size_t bytes) {
 int rp_comm_set_timeout(rp_comm_t c, uint64_t ns) {
   if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_set_timeout: NULL comm");
   c->timeout_ns = ns;
+  return RP_OK;
+}
+
+int rp_comm_set_block_cap(rp_comm_t c, int blocks) {
+  if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_set_block_cap: NULL comm");
+  if (blocks < 0) return rp_fail(RP_ERR_INVALID, "rp_comm_set_block_cap: negative");
+  c->block_cap = blocks;
   return RP_OK;
 }
 

@@ -79,6 +79,7 @@ struct rp_comm {
   uint64_t timeout_ns = 20ull * 1000ull * 1000ull * 1000ull;
   int num_sms = 148;
   int max_coresident = 0;
+  int block_cap = 0;       // >0: at most this many blocks per rank (rp_comm_set_block_cap)
   // BN scratch: per-split f64 partials (device memory, all local replicas)
   double* bn_partials = nullptr;
   size_t bn_partials_bytes = 0;

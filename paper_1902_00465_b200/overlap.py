@@ -96,8 +96,12 @@ class OverlappedReplicatedOptimizer:
     """``wrap_optimizer(opt, overlap=True)`` result: see the module docstring."""
 
     DEFAULT_BUCKET_BYTES = 8 << 20
+    DEFAULT_BLOCKS = 32
 
-    def __init__(self, repl, opt, kind: str = "premean", bucket_bytes: int | None = None):
+    def __init__(self, repl, opt, kind: str = "premean", bucket_bytes: int | None = None,
+                 blocks: int | None = None):
+        """``blocks``: grid cap (blocks per rank) of the exchanges launched during
+        backward, so they leave most SMs to the backward kernels (0: no cap)."""
         if repl.is_virtual or not isinstance(repl.comm, Communicator):
             raise errors.ConfigurationError("overlap=True needs one replica per process (torch.distributed); "
                                             "in-process replicas rendezvous on host threads after backward")
@@ -120,13 +124,15 @@ class OverlappedReplicatedOptimizer:
         for bi, idx in enumerate(plan):
             dt = uniq[idx[0]].dtype
             comm_dt = cdt if (cdt is not None and dt == torch.float32) else dt
-            self.buckets.append(_Bucket(self.comm, [[uniq[i] for i in idx]], dt, comm_dt))
+            self.buckets.append(_Bucket(self.comm, [[uniq[i] for i in idx]], dt, comm_dt,
+                                        views=getattr(repl, "grad_views", True)))
             for i in idx:
                 self._where[id(uniq[i])] = bi
         self._left = [len(idx) for idx in plan]
         self._pending = list(self._left)
         self._order = InOrderLauncher(len(self.buckets))
         self.stream = torch.cuda.Stream(device=self.comm.device, priority=-1)
+        self.blocks = self.DEFAULT_BLOCKS if blocks is None else int(blocks)
         self._sync = True
         self._launched_any = False
         self._steps = 0
@@ -182,12 +188,16 @@ class OverlappedReplicatedOptimizer:
     def _launch(self, i: int):
         b = self.buckets[i]
         self._pending[i] = 0
-        grads = [b._grads(0)]  # dense fix-ups on the compute stream
+        grads = None if b.views else [b._grads(0)]  # dense fix-ups on the compute stream
         cur = torch.cuda.current_stream(self.comm.device)
         self.stream.wait_stream(cur)
-        with torch.cuda.stream(self.stream):
-            b.reduce(self.kind, grads)
-        for g in grads[0]:
+        self.comm.set_block_cap(self.blocks)  # same value on every rank, same position in the sequence
+        try:
+            with torch.cuda.stream(self.stream):
+                b.reduce(self.kind, grads)
+        finally:
+            self.comm.set_block_cap(0)
+        for g in (grads[0] if grads else ()):
             g.record_stream(self.stream)
         self._launched_any = True
 

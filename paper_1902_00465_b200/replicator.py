@@ -182,11 +182,15 @@ class Replicator:
     def __init__(self, num_replicas: int | None = None, *, group=None, device: int | None = None,
                  pool_bytes: int = DEFAULT_POOL_BYTES, timeout_s: float = 20.0,
                  grad_comm_dtype: torch.dtype | None = None, bucket_bytes: int | None = None,
-                 nvls_bytes: int = 0, check_protocol: bool = False):
+                 nvls_bytes: int = 0, check_protocol: bool = False, grad_views: bool = True):
         """``nvls_bytes`` > 0 (multi-process, >= 2 ranks): bind that much memory per
         rank to an NVSwitch multicast region and place gradient fusion buckets in it
         while it has room, so wrap_optimizer's reduction runs in the switch
         (RP_ALGO_NVLS; not rank-ordered -- leave 0 for bit-exact reference parity).
+
+        ``grad_views`` (default): wrap_optimizer's gradients live in the fusion
+        buckets (``param.grad`` is a view of its bucket slot), so the exchange is one
+        in-place all-reduce per bucket with no pack/unpack passes (bucket.py).
 
         ``check_protocol`` (debug): every collective first
         checks that all ranks issue the same (generation, call index, label, kind,
@@ -217,6 +221,7 @@ class Replicator:
         self._generation, self._call_index = 0, 0
         self.grad_comm_dtype = grad_comm_dtype
         self.bucket_bytes = bucket_bytes
+        self.grad_views = grad_views
         self._in_context = False
         self._replicated: list[PerReplica] = []
 
@@ -279,7 +284,8 @@ class Replicator:
                     if self.comm.world > 1:
                         self.comm.broadcast_tensor(tensors[0][k].data, root=0)
 
-    def wrap_optimizer(self, optimizer, kind: str = "premean", fused: bool = False, overlap: bool = False):
+    def wrap_optimizer(self, optimizer, kind: str = "premean", fused: bool = False, overlap: bool = False,
+                       overlap_blocks: int | None = None):
         """apply_gradients first averages every gradient across
         replicas with all_sum(g / R), then applies the base rule.
 
@@ -306,7 +312,7 @@ class Replicator:
             return FusedReplicatedOptimizer(self, opts)
         if overlap:
             from .overlap import OverlappedReplicatedOptimizer
-            return OverlappedReplicatedOptimizer(self, opts[0], kind)
+            return OverlappedReplicatedOptimizer(self, opts[0], kind, blocks=overlap_blocks)
         return ReplicatedOptimizer(self, opts, kind)
 
     # -- run ----------------------------------------------------------------
@@ -470,7 +476,7 @@ class ReplicatedOptimizer:
     def _build(self):
         plists = [self._params(o) for o in self.opts]
         self._buckets = GradBuckets(self.repl.comm, plists, comm_dtype=self.repl.grad_comm_dtype,
-                                    bucket_bytes=self.repl.bucket_bytes)
+                                    bucket_bytes=self.repl.bucket_bytes, views=self.repl.grad_views)
 
     def zero_grad(self, set_to_none: bool = False):
         self.optimizer.zero_grad(set_to_none=set_to_none)

@@ -573,9 +573,9 @@ def body_overlap(rank, world):
 
     for comm_dt in (None, torch.bfloat16):
         results = []
-        for overlap in (False, True):
-            repl = Replicator(device=rank, pool_bytes=32 << 20, grad_comm_dtype=comm_dt,
-                              bucket_bytes=(2 << 10) if overlap else None)
+        for overlap, views in ((False, False), (False, True), (True, True)):
+            repl = Replicator(device=rank, pool_bytes=32 << 20, grad_comm_dtype=comm_dt, grad_views=views,
+                              bucket_bytes=(1 << 10) if overlap else None)
             torch.manual_seed(rank)
             with repl.context():
                 model = repl.replicate(lambda: net().to(memory_format=torch.channels_last))
@@ -583,7 +583,9 @@ def body_overlap(rank, world):
                 params = list(unused.local.parameters()) + list(model.local.parameters())  # unused -> last bucket
                 opt = repl.wrap_optimizer(torch.optim.SGD(params, lr=0.05, momentum=0.9), overlap=overlap)
             if overlap:
-                assert len(opt.buckets) > 3, "small bucket_bytes must give several buckets"
+                assert len(opt.buckets) > 3, ("small bucket_bytes must give several buckets",
+                                              [b.counts for b in opt.buckets], repl.bucket_bytes)
+                assert all(p.grad is not None and b.views for b in opt.buckets for p in b.params[0])
             for step in range(4):
                 g = torch.Generator().manual_seed(10 * step + rank)
                 opt.zero_grad(set_to_none=(step % 2 == 1))
@@ -608,9 +610,10 @@ def body_overlap(rank, world):
                 assert "no_sync" in str(ei.value) or isinstance(ei.value, errors.ProtocolError)
                 opt.remove_hooks()
             repl.comm.close()
-        for a, b in zip(*results):
-            assert torch.equal(a, b), f"overlap differs from the synchronous wrapped optimizer ({comm_dt})"
-        flat = torch.cat([p.reshape(-1) for p in results[1]])
+        for other, what in ((results[1], "gradient views"), (results[2], "overlap")):
+            for a, b in zip(results[0], other):
+                assert torch.equal(a, b), f"{what} differs from the packed synchronous exchange ({comm_dt})"
+        flat = torch.cat([p.reshape(-1) for p in results[2]])
         import torch.distributed as dist
         gl = [torch.empty_like(flat.cpu()) for _ in range(world)]
         dist.all_gather(gl, flat.cpu())

@@ -43,6 +43,8 @@ def main():
     p.add_argument("--overlap", action="store_true",
                    help="wrap_optimizer(overlap=True): buckets exchanged from grad hooks during backward")
     p.add_argument("--bucket-mb", type=float, default=None, help="fusion bucket size (overlap)")
+    p.add_argument("--overlap-blocks", type=int, default=None, help="grid cap of overlapped exchanges (0: none)")
+    p.add_argument("--no-grad-views", action="store_true", help="pack/unpack gradients instead of bucket views")
     a = p.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -61,13 +63,14 @@ def main():
     repl = Replicator(device=local, pool_bytes=512 << 20,
                       grad_comm_dtype=torch.bfloat16 if a.grad_comm == "bf16" else None,
                       nvls_bytes=(128 << 20) if (a.nvls and world > 1) else 0,
-                      bucket_bytes=int(a.bucket_mb * (1 << 20)) if a.bucket_mb else None)
+                      bucket_bytes=int(a.bucket_mb * (1 << 20)) if a.bucket_mb else None,
+                      grad_views=not a.no_grad_views)
     torch.manual_seed(rank)  # replicate() broadcasts replica 0's init
     with repl.context():
         model = repl.replicate(lambda: torchvision.models.resnet50().to(memory_format=torch.channels_last))
         opt = repl.wrap_optimizer(torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9, nesterov=True,
                                                   weight_decay=1e-4), fused=a.fused,
-                                   overlap=a.overlap and world > 1)
+                                   overlap=a.overlap and world > 1, overlap_blocks=a.overlap_blocks)
     net = model.local
     if a.no_average:
         opt.average_gradients = lambda: None
@@ -154,9 +157,10 @@ def main():
         if a.fused:
             grad_bytes = sum(g.grads.numel * g.grads.flat[0].element_size() for g in opt.groups if g is not None)
         elif a.overlap and world > 1:
-            grad_bytes = sum(b.numel * b.flat[0].element_size() for b in opt.buckets)
+            grad_bytes = sum(b.numel * torch.empty((), dtype=b.comm_dtype).element_size() for b in opt.buckets)
         else:
-            grad_bytes = sum(b.numel * b.flat[0].element_size() for b in opt._buckets.buckets) if opt._buckets else 0
+            grad_bytes = sum(b.numel * torch.empty((), dtype=b.comm_dtype).element_size()
+                             for b in opt._buckets.buckets) if opt._buckets else 0
         line = {"metric": "ResNet-50 synthetic img/s", "value": world * a.batch / (ms / 1e3), "unit": "img/s",
                 "n_gpus": world, "per_gpu_batch": a.batch, "ms_per_step": ms, "steps": a.steps, "warmup": a.warmup,
                 "allreduce_ms": ar_ms, "allreduce_share": ar_ms / ms if ms else 0.0,
