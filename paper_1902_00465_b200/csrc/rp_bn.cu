@@ -313,7 +313,33 @@ __global__ void __launch_bounds__(kBnThreads) bn_partial_nchw(const BnArgs a) {
 // partial sums are then folded in lane order through shared memory -- a
 // deterministic order, parallel over the S split partials (a serial loop over S at
 // L2 latency dominated small layers).
-__device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk) {
+// Rank-level barrier of the nblk exchange blocks of this rank, hierarchical like
+// the collectives' phase barriers (rp_device.cuh phase_arrive): every block counts
+// itself in on a LOCAL counter (gpu-scope acq_rel atomic); the last one resets it,
+// issues ONE fence.acq_rel.sys and a relaxed increment of its slot on every rank's
+// BN phase row; all blocks then wait for every rank's slot to reach `target`.
+// The flat form (a release store per block per peer) cost two system-scope fences
+// per block per call: ~27 us for a 4 MiB layer, ncu gpu__time_duration
+// (profiles/r01_bn_bench_clean.txt, before this change).
+__device__ __forceinline__ bool bn_barrier(const ExArgs& a, int rank, int nblk, uint32_t target) {
+  __syncthreads();  // the block's record writes happen-before thread 0's arrival
+  if (threadIdx.x == 0) {
+    uint32_t* ctr = a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + 4 + RP_BN_PHASE;
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    if (old == (uint32_t)nblk - 1) {  // last exchange block of this rank
+      atomicExch(ctr, 0u);            // next barrier counts from 0 (ordered by the fence)
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int p = 0; p < a.world; ++p)
+        asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(
+                         a.t.sig[p] + (size_t)(RP_PH_ROW0 + RP_BN_PHASE) * RP_MAX_RANKS + rank)
+                     : "memory");
+    }
+  }
+  return phase_wait(a.t, a.world, a.timeout_ns, rank, RP_BN_PHASE, target);
+}
+
+__device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk, int nblk) {
   __shared__ double red[kExThreads][2];
   const int rep = a.rank >= 0 ? 0 : rank;  // local replica index
   const int tpc = kExThreads / a.cpb;      // threads per channel
@@ -349,9 +375,10 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
     rec[1] = s2;
     rec[2] = a.local_count[rep];
   }
-  const int es = RP_ST_BN_EPOCH + blk;
-  const uint32_t e0 = epoch_begin(a.t, rank, es);
-  if (!rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blk, e0 + 1)) return;
+  // one rank, one replica: every thread reads back only its own records -- no barrier
+  const bool sync = a.world > 1;
+  const uint32_t seen = sync ? state_load(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE) : 0u;
+  if (sync && !bn_barrier(a, rank, nblk, seen + 1u)) return;
   if (lane == 0 && c < C) {
     double A1 = 0.0, A2 = 0.0, Mt = 0.0;
     for (int p = 0; p < a.world; ++p) {  // ascending rank order
@@ -373,12 +400,14 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
     }
     if (c == 0 && a.count[rep]) *a.count[rep] = Mt;
   }
-  rank_barrier(a.t, a.world, a.timeout_ns, rank, RP_BN_ROW0 + blk, e0 + 2);
-  epoch_end(a.t, rank, es, e0 + 2);
+  if (!sync) return;
+  // records are re-written by the next call: hold every rank until all have read them
+  if (!bn_barrier(a, rank, nblk, seen + 2u)) return;
+  if (blk == 0 && threadIdx.x == 0) state_store(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE, seen + 2u);
 }
 
 __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
-  exchange_body(a, a.rank >= 0 ? a.rank : (int)blockIdx.y, blockIdx.x);
+  exchange_body(a, a.rank >= 0 ? a.rank : (int)blockIdx.y, blockIdx.x, gridDim.x);
 }
 
 // --- fused statistics (NHWC): the local pass and the cross-replica reduction in
@@ -417,7 +446,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_stats_fused(const FusedBnArgs f
   }
   __syncthreads();
   if ((int)bid >= f.ex_blocks) return;
-  exchange_body(f.e, rank, (int)bid);
+  exchange_body(f.e, rank, (int)bid, f.ex_blocks);
   if (bid == 0 && threadIdx.x == 0) state_store(f.e.t, rank, RP_ST_BN_GRID_BASE, base + total);
 }
 

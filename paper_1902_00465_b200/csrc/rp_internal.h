@@ -21,6 +21,8 @@
 #define RP_PH_ROW0 (RP_BN_ROW0 + RP_BN_ROWS)
 #define RP_PH_ROWS 4
 #define RP_CTR_ROW (RP_PH_ROW0 + RP_PH_ROWS)
+// phase row 3 (and local arrival word 4 + 3) belongs to the BN exchange barrier
+#define RP_BN_PHASE 3
 #define RP_ABORT_WORD ((RP_CTR_ROW + 4) * RP_MAX_RANKS)  // u32 index
 // Device-side sequencing state, local to each rank (never written by peers), in
 // the last 16 KiB of the signal region. Kernels read it at start and advance it

@@ -99,7 +99,7 @@ class OverlappedReplicatedOptimizer:
     DEFAULT_BLOCKS = 32
 
     def __init__(self, repl, opt, kind: str = "premean", bucket_bytes: int | None = None,
-                 blocks: int | None = None):
+                 blocks: int | None = None, priority: int = -1):
         """``blocks``: grid cap (blocks per rank) of the exchanges launched during
         backward, so they leave most SMs to the backward kernels (0: no cap)."""
         if repl.is_virtual or not isinstance(repl.comm, Communicator):
@@ -131,7 +131,7 @@ class OverlappedReplicatedOptimizer:
         self._left = [len(idx) for idx in plan]
         self._pending = list(self._left)
         self._order = InOrderLauncher(len(self.buckets))
-        self.stream = torch.cuda.Stream(device=self.comm.device, priority=-1)
+        self.stream = torch.cuda.Stream(device=self.comm.device, priority=priority)
         self.blocks = self.DEFAULT_BLOCKS if blocks is None else int(blocks)
         self._sync = True
         self._launched_any = False

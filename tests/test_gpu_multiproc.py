@@ -377,7 +377,8 @@ def body_wrap_nvls(rank, world):
         torch.nn.functional.cross_entropy(ref(xs.double()), ys).backward()
         ref_opt.step()
     bk = opt._buckets.buckets[0]
-    assert repl.comm.algorithm_for(bk.flat[0], "premean", out=bk.flat[0]) == ("nvls" if world >= 4 else "twoshot")
+    algo = repl.comm.algorithm_for(bk.flat[0], "premean", out=bk.flat[0])
+    assert algo == "nvls" if world >= 4 else algo in ("oneshot", "twoshot")
     for p, q in zip(model.local.parameters(), ref.parameters()):
         assert (p.double() - q).abs().max().item() < 1e-5
     flat = torch.cat([p.detach().reshape(-1) for p in model.local.parameters()])
@@ -575,7 +576,7 @@ def body_overlap(rank, world):
         results = []
         for overlap, views in ((False, False), (False, True), (True, True)):
             repl = Replicator(device=rank, pool_bytes=32 << 20, grad_comm_dtype=comm_dt, grad_views=views,
-                              bucket_bytes=(1 << 10) if overlap else None)
+                              bucket_bytes=256 if overlap else None)
             torch.manual_seed(rank)
             with repl.context():
                 model = repl.replicate(lambda: net().to(memory_format=torch.channels_last))

@@ -45,6 +45,9 @@ def main():
     p.add_argument("--bucket-mb", type=float, default=None, help="fusion bucket size (overlap)")
     p.add_argument("--overlap-blocks", type=int, default=None, help="grid cap of overlapped exchanges (0: none)")
     p.add_argument("--no-grad-views", action="store_true", help="pack/unpack gradients instead of bucket views")
+    p.add_argument("--overlap-priority", type=int, default=-1, help="side-stream priority (-1 high, 0 normal)")
+    p.add_argument("--overlap-dry", action="store_true",
+                   help="diagnostic: hooks and bucket bookkeeping only, no exchange (measures the hook overhead)")
     a = p.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -72,6 +75,11 @@ def main():
                                                   weight_decay=1e-4), fused=a.fused,
                                    overlap=a.overlap and world > 1, overlap_blocks=a.overlap_blocks)
     net = model.local
+    if a.overlap and world > 1:
+        opt.stream = torch.cuda.Stream(device=dev, priority=a.overlap_priority)
+        if a.overlap_dry:
+            for b in opt.buckets:
+                b.reduce = lambda kind, grads=None: None
     if a.no_average:
         opt.average_gradients = lambda: None
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
