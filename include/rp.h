@@ -68,7 +68,10 @@ enum {
   RP_ALGO_NVLS = 3,    /* all_reduce in the NVSwitch (multimem), in place in the NVLS
                           region; NOT rank-ordered: ~1e-6 relative. AUTO picks it
                           for in-place f32/bf16/f16 sum/mean/premean of >= 512 KiB
-                          inside the NVLS region at world >= 4 (RP_NVLS=0: never) */
+                          inside the NVLS region at world >= 4 (RP_NVLS=0: never).
+                          broadcast: dst inside the NVLS region (16-byte multiple):
+                          the root's multicast store reaches every rank (bit-exact);
+                          AUTO picks it whenever dst lies in the region */
 };
 
 /* Status codes -> reference exception (errors.py). */

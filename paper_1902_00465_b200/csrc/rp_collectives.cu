@@ -592,6 +592,17 @@ int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, si
     vec = vec && ((uintptr_t)dst[i] % 16 == 0);
     in_place = in_place && (src[i] == dst[i]);
   }
+  // NVLS: destination placed in the multicast region (symmetric on every rank, so
+  // every rank makes the same choice); the root multicasts from any local source
+  if (!c->is_virtual && W >= 2 && (algo == RP_ALGO_NVLS || algo == RP_ALGO_AUTO)) {
+    const char* ne = getenv("RP_NVLS");
+    // (a property of dst alone, which is symmetric: every rank decides alike)
+    const bool nvls_ok = rp_nvls_covers(c, dst[0], bytes) && bytes % 16 == 0;
+    if (algo == RP_ALGO_NVLS || (nvls_ok && !(ne && ne[0] == '0')))
+      return rp_nvls_bcast_launch(c, src[0], dst[0], bytes, root, stream, dyn_launch, a);
+  } else if (algo == RP_ALGO_NVLS) {
+    return rp_fail(RP_ERR_CONFIG, "broadcast(nvls): needs a multi-process communicator");
+  }
   size_t doff = 0;
   if (in_place && symmetric_in_pool(c, (const void* const*)dst, bytes, &doff)) {
     a.copy_in = 0;

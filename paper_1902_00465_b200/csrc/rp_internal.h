@@ -178,5 +178,8 @@ bool rp_nvls_covers(rp_comm* c, const void* p, size_t bytes);
 // Algorithm rp_all_reduce runs (AUTO resolved): RP_ALGO_ONESHOT / TWOSHOT / NVLS
 int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
                        int dtype_comm, int dtype_out, int op, int algo);
+int rp_nvls_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, cudaStream_t stream,
+                         int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t),
+                         CollArgs& a);
 int rp_nvls_launch(rp_comm* c, const void* buf, size_t count, int dtype, int op, cudaStream_t stream,
                    int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t), CollArgs& a);

@@ -412,9 +412,76 @@ __global__ void __launch_bounds__(kNvlsThreads) ar_nvls(const CollArgs a) {
   rp_trace(a, 7);
 }
 
+// ===========================================================================
+// K4n: NVLS broadcast (destination in the multicast-bound region)
+//   barrier 0 (every rank is done with the destination's previous contents)
+//   root only, per-warp tiles: v = its local source (any local buffer),
+//     multimem.st(mc + v): the switch writes the same 16 bytes into every rank's copy
+//   barrier 1 (the root's stores landed everywhere)
+// Root egress S and every rank's ingress S -- the broadcast lower bound, with no
+// relay step (the P2P scatter + all-gather moves 2(N-1)/N*S through every link).
+// A copy, so bit-exact (graph.py:538-540 pick0).
+// ===========================================================================
+template <bool ROOT_UNUSED = false>
+__global__ void __launch_bounds__(kNvlsThreads) bcast_nvls(const CollArgs a) {
+  const int rank = a.rank;
+  char* mc = (char*)a.dst[rank];  // multicast view of the destination
+  const char* src = (const char*)a.src[rank];
+  const size_t V = a.count / 16;
+  constexpr uint32_t tv = 32 * kNvlsU;
+  const uint32_t nt = (uint32_t)((V + tv - 1) / tv);
+  const int lane = threadIdx.x & 31;
+  rp_trace(a, 0);
+  const PhaseBase pb = phase_begin(a, rank);
+  if (!phase_end(a, rank, 0, pb)) return;
+  if (rank == a.root) {
+    uint32_t j = claim_tile(a, rank, 1);
+    while (j < nt) {
+      const uint32_t next = claim_tile(a, rank, 1);
+      const size_t lo = (size_t)j * tv + lane;
+      uint4 r[kNvlsU];
+#pragma unroll
+      for (int u = 0; u < kNvlsU; ++u) {
+        const size_t v = lo + (size_t)u * 32;
+        if (v < V) r[u] = ld128_stream(src + v * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < kNvlsU; ++u) {
+        const size_t v = lo + (size_t)u * 32;
+        if (v < V) mc_st(mc + v * 16, r[u]);
+      }
+      j = next;
+    }
+  }
+  if (!phase_end(a, rank, 1, pb)) return;
+  dyn_finish(a, rank, 2, pb);
+  rp_trace(a, 7);
+}
+
 }  // namespace rp
 
 using namespace rp;
+
+int rp_nvls_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, cudaStream_t stream,
+                         int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t),
+                         CollArgs& a) {
+  NvlsState* s = nvls_of(c);
+  if (!s || !s->bound) return rp_fail(RP_ERR_CONFIG, "broadcast(nvls): NVLS region not set up");
+  if (!rp_nvls_covers(c, dst, bytes) || bytes % 16)
+    return rp_fail(RP_ERR_INVALID, "broadcast(nvls): dst must be a 16-byte multiple inside the NVLS region");
+  if (c->rank == root && ((uintptr_t)src % 16)) {  // misaligned source: multicast from dst
+    RP_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, stream));
+    src = dst;
+  }
+  const size_t off = (size_t)((const char*)dst - (const char*)s->uc_va);
+  a.count = bytes;
+  a.root = root;
+  a.chunk = bytes / 16;
+  a.src[c->rank] = src;
+  a.dst[c->rank] = (void*)(s->mc_va + off);
+  a.copy_in = a.copy_out = 0;
+  return dyn(c, (const void*)bcast_nvls<false>, a, stream, "bcast_nvls", c->num_sms, kNvlsThreads, 32 * kNvlsU);
+}
 
 int rp_nvls_launch(rp_comm* c, const void* buf, size_t count, int dtype, int op, cudaStream_t stream,
                    int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t), CollArgs& a) {

@@ -341,6 +341,26 @@ def body_nvls(rank, world):
     want = np.sum(np.stack(xs).astype(np.float64), axis=0) / world
     got = big.cpu().numpy().astype(np.float64)
     assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-6
+    # NVLS broadcast (rp.h RP_ALGO_NVLS for rp_broadcast): destination in the region,
+    # the root multicasts from any local source (in place, separate, misaligned); bit-exact
+    dev = torch.device(f"cuda:{rank}")
+    for nbytes in (16, 4096, (1 << 20) + 48, 7 << 20):
+        for root in (0, world - 1):
+            want = torch.from_numpy(np.random.default_rng(nbytes + root).integers(0, 256, nbytes + 1, dtype=np.uint8))
+            dst = comm.alloc_nvls(nbytes, torch.uint8)
+            dst.fill_(rank + 1)
+            src = want.to(dev)
+            for mode in ("in_place", "separate", "misaligned"):
+                if mode == "in_place":
+                    if rank == root:
+                        dst.copy_(src[:nbytes])
+                    comm.broadcast_tensor(dst, root=root)
+                else:
+                    s0 = src[:nbytes] if mode == "separate" else src[1:nbytes + 1]
+                    comm.broadcast_tensor(s0, root=root, out=dst)
+                exp = want[:nbytes] if mode != "misaligned" else want[1:nbytes + 1]
+                assert torch.equal(dst.cpu(), exp), (nbytes, root, mode)
+                dst.fill_(rank + 7)
     comm.check()
     comm.close()
 

@@ -75,6 +75,8 @@ def main():
                                                                 else ["auto"])
         if "nccl" in a.algos.split(",") and op != "all_reduce":
             algos = algos + ["nccl"]  # comparison column only: NCCL is never on the product path
+        if "nvls" in a.algos.split(",") and op == "broadcast":
+            algos = algos + ["nvls"]  # in place in the NVLS region: the root's multicast store
         for lg in range(a.min_log2, a.max_log2 + 1):
             size = 1 << lg
             count = size // 4
@@ -115,6 +117,10 @@ def main():
                         if world == 1:
                             continue
                         fn = lambda: torch.distributed.broadcast(os_[0], src=0)  # noqa: E731
+                    elif algo == "nvls":
+                        if nvls_buf is None:
+                            continue
+                        fn = lambda: comm.broadcast_tensor(nvls_buf[:count], root=0)  # noqa: E731
                     elif world == 1:
                         fn = lambda: comm.broadcast(xs, root=0, outs=os_, algo=algo)  # noqa: E731
                     else:
