@@ -99,6 +99,41 @@ __global__ void __launch_bounds__(kThreads) allgather_kernel(const CollArgs a, s
   epoch_end(a.t, rank, es, e0 + 2);
 }
 
+// K3p: one-shot all_gather, push form (multi-process, small messages, ONE barrier):
+// every rank stores its src into slot [rank] of every peer's one-shot landing zone
+// (and straight into its own dst slot), meets its peers once, then copies the
+// received slots into dst locally. The zone alternates by call parity exactly as
+// for the push one-shot all-reduce (same zones, same parity state), so no trailing
+// barrier is needed. a.read_off = parity-0 zone, a.chunk = slot stride (16-B
+// multiple, slots * world <= RP_OS_REGION), a.write_off = per-block byte slice.
+__global__ void __launch_bounds__(kThreads) allgather_push_kernel(const CollArgs a, int vec) {
+  const int rank = a.rank;
+  const size_t B = a.count;
+  const size_t lo = (size_t)blockIdx.x * a.write_off;
+  const size_t hi = std::min(lo + a.write_off, B);
+  const int es = RP_ST_BLK_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
+  const size_t zone = a.read_off + (size_t)zone_parity_begin(a.t, rank) * RP_OS_REGION;
+  const char* src = (const char*)a.src[rank];
+  char* dst = (char*)a.dst[rank];
+  if (lo < hi) {
+    for (int i = 1; i < a.world; ++i) {
+      const int p = (rank + i) % a.world;
+      copy_bytes(a.t.data[p] + zone + (size_t)rank * a.chunk, src, lo, hi, vec);
+    }
+    if (dst + (size_t)rank * B != src) copy_bytes(dst + (size_t)rank * B, src, lo, hi, vec);
+  }
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 1)) return;
+  epoch_end(a.t, rank, es, e0 + 1);
+  if (lo < hi) {
+    const char* z = a.t.data[rank] + zone;
+    for (int i = 1; i < a.world; ++i) {
+      const int p = (rank + i) % a.world;
+      copy_bytes(dst + (size_t)p * B, z + (size_t)p * a.chunk, lo, hi, vec);
+    }
+  }
+}
+
 // K4a: direct broadcast: every rank pulls root's pool copy.
 __global__ void __launch_bounds__(kThreads) bcast_direct_kernel(const CollArgs a, int vec) {
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
@@ -540,6 +575,21 @@ int rp_launch_all_gather(rp_comm* c, const void* const* src, void* const* dst, s
     vec = vec && ((uintptr_t)src[i] % 16 == 0) && ((uintptr_t)dst[i] % 16 == 0);
   const size_t scratch = round_up(c->reserved, RP_ALIGN);
   const size_t scratch_end = c->scratch_end();
+  // small messages between processes: push into the peers' landing zones, one
+  // barrier (K3p); the bound keeps world slots inside one zone
+  const size_t slot = round_up(bytes, 16);
+  if (!c->is_virtual && W > 1 && slot * W <= RP_OS_REGION && slot <= ((size_t)256 << 10) &&
+      getenv("RP_AG_PULL") == nullptr) {
+    a.read_off = c->oneshot_zone(0);
+    a.chunk = slot;
+    const size_t per_block_min = (size_t)16 * kThreads * 2;
+    const int want = (int)std::min<size_t>((bytes + per_block_min - 1) / per_block_min, (size_t)RP_MAX_BLOCKS);
+    const int blocks = rp_blocks_per_rank(c, (const void*)allgather_push_kernel, kThreads, std::max(want, 1));
+    a.write_off = round_up((bytes + blocks - 1) / blocks, 16);
+    int ivec = vec ? 1 : 0;
+    void* args[] = {&a, &ivec};
+    return rp_launch(c, (const void*)allgather_push_kernel, dim3(blocks), dim3(kThreads), args, 0, stream);
+  }
   bool in_place = true;
   for (int i = 0; i < nrep && in_place; ++i) {
     const int r = c->is_virtual ? i : c->rank;

@@ -116,11 +116,16 @@ def body_gather_broadcast(rank, world):
     from paper_1902_00465_b200.comm import Communicator
 
     dev = torch.device(f"cuda:{rank}")
-    comm = Communicator(device=rank, pool_bytes=64 << 20)
-    for count in (1, 7, 1000, 12345, 1 << 20):
+    comm = Communicator(device=rank, pool_bytes=96 << 20)
+    for count in (1, 7, 1000, 12345, 65536, 65537, 1 << 20):
         xs = _inputs(world, count, seed=count + 1)
         g = comm.all_gather_tensor(torch.from_numpy(xs[rank]).to(dev))
         assert g.cpu().numpy().tobytes() == np.concatenate(xs).tobytes()
+        # in place: src is this rank's slot of a pool-resident output
+        out = comm.alloc(world * count, torch.float32).view(world, count)
+        out[rank].copy_(torch.from_numpy(xs[rank]))
+        comm.all_gather_tensor(out[rank], out=out)
+        assert out.cpu().numpy().tobytes() == np.concatenate(xs).tobytes(), count
         for root in range(world):
             for algo in ("direct", "scatter"):
                 x = torch.from_numpy(xs[rank]).to(dev)
