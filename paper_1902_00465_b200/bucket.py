@@ -137,12 +137,19 @@ class _Bucket:
                                    gcode, stream), "pack")
         return grads
 
-    def reduce(self, kind: str, grads=None):
+    def is_attached(self, r: int, k: int) -> bool:
+        """(views) replica r's k-th gradient is its bucket slot."""
+        g, v = self.params[r][k].grad, self.slots[r][k]
+        return g is not None and g.data_ptr() == v.data_ptr() and g.stride() == v.stride()
+
+    def reduce(self, kind: str, grads=None, attached: bool = False):
         """pack -> in-place premean/sum fold -> unpack, all on the current stream
-        (views: attach, then the in-place fold with the cast fused)."""
+        (views: attach -- skipped when the caller checked every gradient already --
+        then the in-place fold with the cast fused)."""
         if self.views:
-            with torch.no_grad():
-                self.attach()
+            if not attached:
+                with torch.no_grad():
+                    self.attach()
             cdt = None if self.comm_dtype == self.grad_dtype else self.comm_dtype
             if isinstance(self.comm, VirtualCommunicator):
                 self.comm.all_reduce(self.flat, kind, outs=self.flat, comm_dtype=cdt)

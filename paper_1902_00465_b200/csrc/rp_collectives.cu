@@ -134,6 +134,29 @@ __global__ void __launch_bounds__(kThreads) allgather_push_kernel(const CollArgs
   }
 }
 
+// K4p: one-shot broadcast, push form (multi-process, small messages, ONE barrier):
+// the root stores its src into every peer's one-shot landing zone (and its own
+// dst), all ranks meet once, every non-root copies the zone into its dst. Same
+// zones and parity protocol as K1p / K3p. a.write_off = per-block byte slice.
+__global__ void __launch_bounds__(kThreads) bcast_push_kernel(const CollArgs a, int vec) {
+  const int rank = a.rank;
+  const size_t B = a.count;
+  const size_t lo = (size_t)blockIdx.x * a.write_off;
+  const size_t hi = std::min(lo + a.write_off, B);
+  const int es = RP_ST_BLK_EPOCH + blockIdx.x;
+  const uint32_t e0 = epoch_begin(a.t, rank, es);
+  const size_t zone = a.read_off + (size_t)zone_parity_begin(a.t, rank) * RP_OS_REGION;
+  char* dst = (char*)a.dst[rank];
+  if (rank == a.root && lo < hi) {
+    const char* src = (const char*)a.src[rank];
+    for (int i = 1; i < a.world; ++i) copy_bytes(a.t.data[(rank + i) % a.world] + zone, src, lo, hi, vec);
+    if (dst != src) copy_bytes(dst, src, lo, hi, vec);
+  }
+  if (!rank_barrier(a, rank, blockIdx.x, e0, 1)) return;
+  epoch_end(a.t, rank, es, e0 + 1);
+  if (rank != a.root && lo < hi) copy_bytes(dst, a.t.data[rank] + zone, lo, hi, vec);
+}
+
 // K4a: direct broadcast: every rank pulls root's pool copy.
 __global__ void __launch_bounds__(kThreads) bcast_direct_kernel(const CollArgs a, int vec) {
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
@@ -578,7 +601,7 @@ int rp_launch_all_gather(rp_comm* c, const void* const* src, void* const* dst, s
   // small messages between processes: push into the peers' landing zones, one
   // barrier (K3p); the bound keeps world slots inside one zone
   const size_t slot = round_up(bytes, 16);
-  if (!c->is_virtual && W > 1 && slot * W <= RP_OS_REGION && slot <= ((size_t)256 << 10) &&
+  if (!c->is_virtual && W > 1 && slot * W <= RP_OS_REGION && slot <= ((size_t)1 << 20) &&
       getenv("RP_AG_PULL") == nullptr) {
     a.read_off = c->oneshot_zone(0);
     a.chunk = slot;
@@ -652,6 +675,19 @@ int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, si
       return rp_nvls_bcast_launch(c, src[0], dst[0], bytes, root, stream, dyn_launch, a);
   } else if (algo == RP_ALGO_NVLS) {
     return rp_fail(RP_ERR_CONFIG, "broadcast(nvls): needs a multi-process communicator");
+  }
+  // small messages between processes: the root pushes into the peers' landing zones
+  // (K4p), one barrier
+  if (!c->is_virtual && W > 1 && algo == RP_ALGO_AUTO && bytes <= std::min(RP_OS_REGION, (size_t)1 << 20) &&
+      getenv("RP_BCAST_PULL") == nullptr) {
+    a.read_off = c->oneshot_zone(0);
+    const size_t per_block_min = (size_t)16 * kThreads * 2;
+    const int want = (int)std::min<size_t>((bytes + per_block_min - 1) / per_block_min, (size_t)RP_MAX_BLOCKS);
+    const int blocks = rp_blocks_per_rank(c, (const void*)bcast_push_kernel, kThreads, std::max(want, 1));
+    a.write_off = round_up((bytes + blocks - 1) / blocks, 16);
+    int ivec = vec ? 1 : 0;
+    void* args[] = {&a, &ivec};
+    return rp_launch(c, (const void*)bcast_push_kernel, dim3(blocks), dim3(kThreads), args, 0, stream);
   }
   size_t doff = 0;
   if (in_place && symmetric_in_pool(c, (const void* const*)dst, bytes, &doff)) {

@@ -30,6 +30,7 @@ protocol error (the averaged value would be overwritten by a local one).
 from __future__ import annotations
 
 import contextlib
+import time
 
 import torch
 
@@ -121,19 +122,24 @@ class OverlappedReplicatedOptimizer:
         plan = bucket_plan(esz, [p.dtype for p in uniq], limit)
         self.buckets: list[_Bucket] = []
         self._where: dict[int, int] = {}
+        self._slot: dict[int, int] = {}
         for bi, idx in enumerate(plan):
             dt = uniq[idx[0]].dtype
             comm_dt = cdt if (cdt is not None and dt == torch.float32) else dt
             self.buckets.append(_Bucket(self.comm, [[uniq[i] for i in idx]], dt, comm_dt,
                                         views=getattr(repl, "grad_views", True)))
-            for i in idx:
+            for k, i in enumerate(idx):
                 self._where[id(uniq[i])] = bi
+                self._slot[id(uniq[i])] = k
         self._left = [len(idx) for idx in plan]
         self._pending = list(self._left)
+        self._detached = [False] * len(self.buckets)  # a gradient stopped being its bucket view
+        self.hook_s = 0.0  # host seconds spent in the hooks (diagnostics)
         self._order = InOrderLauncher(len(self.buckets))
         self.stream = torch.cuda.Stream(device=self.comm.device, priority=priority)
         self.blocks = self.DEFAULT_BLOCKS if blocks is None else int(blocks)
         self._sync = True
+        self._draining = False
         self._launched_any = False
         self._steps = 0
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in uniq]
@@ -175,11 +181,21 @@ class OverlappedReplicatedOptimizer:
     def _on_grad(self, p):
         if not self._sync or self.repl.num_replicas == 1:
             return
+        t0 = time.perf_counter()
+        try:
+            self._ready(p)
+        finally:
+            self.hook_s += time.perf_counter() - t0
+
+    def _ready(self, p):
         bi = self._where[id(p)]
         if self._pending[bi] == 0:
             raise errors.ProtocolError(
                 f"a gradient of bucket {bi} was accumulated again after the bucket was exchanged; "
                 "wrap all but the last backward of an accumulation in opt.no_sync()")
+        b = self.buckets[bi]
+        if b.views and not b.is_attached(0, self._slot[id(p)]):
+            self._detached[bi] = True
         self._pending[bi] -= 1
         if self._pending[bi] == 0:
             for i in self._order.mark(bi):
@@ -194,7 +210,9 @@ class OverlappedReplicatedOptimizer:
         self.comm.set_block_cap(self.blocks)  # same value on every rank, same position in the sequence
         try:
             with torch.cuda.stream(self.stream):
-                b.reduce(self.kind, grads)
+                # gradients checked one by one in the hooks: attach only when one moved
+                attached = b.views and self._pending[i] == 0 and not self._detached[i] and not self._draining
+                b.reduce(self.kind, grads, attached=attached)
         finally:
             self.comm.set_block_cap(0)
         for g in (grads[0] if grads else ()):
@@ -206,11 +224,16 @@ class OverlappedReplicatedOptimizer:
         stream wait for every exchange of this step."""
         if self.repl.num_replicas == 1:
             return
-        for i in self._order.rest():
-            self._launch(i)
+        self._draining = True  # buckets backward did not complete: attach everything
+        try:
+            for i in self._order.rest():
+                self._launch(i)
+        finally:
+            self._draining = False
         torch.cuda.current_stream(self.comm.device).wait_stream(self.stream)
         self._order.reset()
         self._pending = list(self._left)
+        self._detached = [False] * len(self.buckets)
 
     def step(self, closure=None):
         self.average_gradients()

@@ -127,7 +127,7 @@ def body_gather_broadcast(rank, world):
         comm.all_gather_tensor(out[rank], out=out)
         assert out.cpu().numpy().tobytes() == np.concatenate(xs).tobytes(), count
         for root in range(world):
-            for algo in ("direct", "scatter"):
+            for algo in ("auto", "direct", "scatter"):
                 x = torch.from_numpy(xs[rank]).to(dev)
                 comm.broadcast_tensor(x, root=root, algo=algo)
                 assert x.cpu().numpy().tobytes() == xs[root].tobytes(), (count, root, algo)

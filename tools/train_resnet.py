@@ -128,6 +128,7 @@ def main():
         torch.distributed.barrier()
     stream = torch.cuda.current_stream(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    hook0 = getattr(opt, "hook_s", 0.0)
     t0 = time.time()
     for e0, e1 in evs:
         e0.record(stream)
@@ -135,6 +136,7 @@ def main():
         e1.record(stream)
     torch.cuda.synchronize()
     wall = time.time() - t0
+    hook_ms = (getattr(opt, "hook_s", 0.0) - hook0) * 1e3 / a.steps
     ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in evs)
     # the gradient all-reduce alone (same buckets), for its share of the step
     ar_ms = 0.0
@@ -174,7 +176,7 @@ def main():
                 "allreduce_ms": ar_ms, "allreduce_share": ar_ms / ms if ms else 0.0,
                 "grad_exchange_bytes": grad_bytes, "grad_comm": a.grad_comm, "replicas_identical": consistent,
                 "loss": float(loss.item()), "wall_s": wall, "fused_apply": a.fused, "nvls": a.nvls,
-                "overlap": a.overlap, "buckets": len(opt.buckets) if (a.overlap and world > 1) else None,
+                "overlap": a.overlap, "overlap_hook_host_ms": hook_ms, "buckets": len(opt.buckets) if (a.overlap and world > 1) else None,
                 "config": {"model": "resnet50 (torchvision, random init)", "input": "synthetic 224x224x3 channels_last",
                            "precision": "bf16 autocast, fp32 master", "optimizer": "SGD nesterov 0.9 wd 1e-4"}}
         print(json.dumps(line), flush=True)
