@@ -348,26 +348,20 @@ def run_ours(args, rank, world, local):
 
 
 def run_e2e(args, comm, world, n, count, dev, stream):
+    """The same metric through the public host-buffer API: pinned host tensors in,
+    pinned host tensor out (Communicator / VirtualCommunicator.all_reduce_host,
+    which pipelines chunks through pool-resident device slots so the host->device
+    copies, the exchange and the device->host copy overlap)."""
     import torch
 
     k = max(1, args.e2e_steps)
     reps = n if world == 1 else 1
     host_in = [torch.randn(count).pin_memory() for _ in range(reps)]
     host_out = torch.empty(count).pin_memory()
-    if getattr(args, "use_nvls", False):  # the in-switch path reduces in place in the multicast region
-        dev_in = [comm.alloc_nvls(count, torch.float32)]
-    else:
-        dev_in = [torch.empty(count, device=dev) for _ in range(reps)]
+    nvls = bool(getattr(args, "use_nvls", False))
 
     def step():
-        for h, d in zip(host_in, dev_in):
-            d.copy_(h, non_blocking=True)
-        if world == 1:
-            outs = comm.all_reduce(dev_in, args.kind, outs=dev_in, algo=args.algo)
-            host_out.copy_(outs[0], non_blocking=True)
-        else:
-            comm.all_reduce_tensor(dev_in[0], args.kind, out=dev_in[0], algo=args.algo)
-            host_out.copy_(dev_in[0], non_blocking=True)
+        comm.all_reduce_host(host_in if world == 1 else host_in[0], args.kind, host_out=host_out, nvls=nvls)
 
     step()
     torch.cuda.synchronize()
@@ -382,9 +376,8 @@ def run_e2e(args, comm, world, n, count, dev, stream):
     ms = max_over_ranks(a.elapsed_time(b) / k, world)
     return {"value": busbw(args.bytes, n, ms / 1e3) * world, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": reps * count * 4, "d2h_bytes_per_step": count * 4,
-            "path": "pinned host -> cudaMemcpyAsync -> rp_all_reduce(_v) -> host (" +
-                    ("in place in the NVLS region" if getattr(args, "use_nvls", False) else
-                     "staged, non-pool buffers") + ")"}
+            "path": "pinned host -> all_reduce_host (chunks: cudaMemcpyAsync H2D | rp_all_reduce(_v) in place "
+                    "in pool slots | D2H, overlapped) -> pinned host" + (" [NVLS slots]" if nvls else "")}
 
 
 def main():

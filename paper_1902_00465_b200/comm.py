@@ -130,6 +130,88 @@ class _Base:
         cap). Set identically on every rank (include/rp.h rp_comm_set_block_cap)."""
         _lib.check(self._lib.rp_comm_set_block_cap(self._handle, int(blocks)), "set_block_cap")
 
+    # -- host buffers in, host buffer out ------------------------------------
+    HOST_CHUNK_BYTES = 8 << 20
+    HOST_RING = 3
+
+    def all_reduce_host(self, host_in, kind: str = "sum", host_out: torch.Tensor | None = None,
+                        chunk_bytes: int | None = None, nvls: bool = False) -> torch.Tensor:
+        """Host tensors in, host tensor out, pipelined (the path a reference caller
+        with numpy/CPU data takes, graph.py:571-574): the message is cut into chunks
+        that flow through a ring of pool-resident device slots -- chunk i's
+        host->device copies on one stream, its in-place all-reduce on the current
+        stream, its device->host copy on a third -- so both PCIe directions and the
+        exchange overlap instead of running back to back.
+
+        ``host_in``: this rank's CPU tensor (multi-process), or one per replica
+        (virtual). Pinned memory gives asynchronous copies. ``host_out`` receives the
+        result (replica 0's for a virtual communicator: all replicas hold the same
+        bits). Same arithmetic as all_reduce_tensor on the whole message (the folds
+        are elementwise). ``nvls=True`` (multi-process, opt-in like Replicator's
+        nvls_bytes): the device slots live in the NVLS region, so chunks of >= 512 KiB
+        reduce in the switch at >= 4 ranks (not rank-ordered). Returns host_out after
+        the copies completed."""
+        ins = list(host_in) if isinstance(host_in, (list, tuple)) else [host_in]
+        nrep = self.world if isinstance(self, VirtualCommunicator) else 1
+        if len(ins) != nrep:
+            raise errors.ShapeError(f"expected {nrep} host tensors, got {len(ins)}")
+        x0 = ins[0]
+        for x in ins:
+            if x.device.type != "cpu" or x.dtype != x0.dtype or x.numel() != x0.numel():
+                raise errors.ProtocolError("all_reduce_host: CPU tensors of one dtype and size")
+        ins = [x.reshape(-1) if x.is_contiguous() else x.contiguous().reshape(-1) for x in ins]
+        n, dt = x0.numel(), x0.dtype
+        if host_out is None:
+            host_out = torch.empty(n, dtype=dt, pin_memory=ins[0].is_pinned())
+        out = host_out.reshape(-1)
+        esz = x0.element_size()
+        ce = max(16 // esz, min(n, (chunk_bytes or self.HOST_CHUNK_BYTES) // esz)) if n else 1
+        dev = torch.device(f"cuda:{self.device}")
+        ring = self._host_ring(ce, dt, nvls)
+        cur = torch.cuda.current_stream(dev)
+        h2d, d2h = self._host_streams
+        free = [None] * len(ring)
+        starts = list(range(0, n, ce))
+        for i, lo in enumerate(starts):
+            hi = min(lo + ce, n)
+            s = i % len(ring)
+            bufs = ring[s]
+            with torch.cuda.stream(h2d):
+                if free[s] is not None:
+                    h2d.wait_event(free[s])  # the slot's previous chunk has left for the host
+                for r in range(nrep):
+                    bufs[r][: hi - lo].copy_(ins[r][lo:hi], non_blocking=True)
+            cur.wait_stream(h2d)
+            views = [b[: hi - lo] for b in bufs]
+            if nrep > 1:
+                self.all_reduce(views, kind, outs=views)
+            else:
+                self.all_reduce_tensor(views[0], kind, out=views[0])
+            d2h.wait_stream(cur)
+            with torch.cuda.stream(d2h):
+                out[lo:hi].copy_(views[0], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(d2h)
+                free[s] = ev
+        cur.wait_stream(d2h)
+        cur.synchronize()
+        return host_out
+
+    def _host_ring(self, chunk_elems: int, dtype: torch.dtype, nvls: bool = False):
+        """Pool-resident device slots for all_reduce_host, allocated once per (size,
+        dtype, placement) -- symmetrically, since every rank makes the same calls."""
+        key = (chunk_elems, dtype, nvls)
+        rings = self.__dict__.setdefault("_rings", {})
+        if key not in rings:
+            slots = []
+            for _ in range(self.HOST_RING):
+                b = self.alloc_nvls(chunk_elems, dtype) if nvls else self.alloc(chunk_elems, dtype)
+                slots.append(b if isinstance(b, list) else [b])
+            rings[key] = slots
+            dev = torch.device(f"cuda:{self.device}")
+            self._host_streams = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
+        return rings[key]
+
     # -- label protocol (SPEC.md:182-186, :236) -----------------------------
     def new_generation(self):
         """Start a new generation (training step): labels may be reused again."""

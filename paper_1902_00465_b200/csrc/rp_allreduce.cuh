@@ -11,6 +11,13 @@ namespace rp {
 
 constexpr int kThreads = 512;
 constexpr int kUnroll = 2;
+// two resident 512-thread blocks per SM (<= 64 registers): 32 warps of loads in
+// flight instead of 16 (ncu: 1 block/SM at 68-84 registers, 25% occupancy,
+// long-scoreboard bound; profiles/r01_ncu_ar_twoshot_dyn_n1.txt)
+#ifndef RP_TWOSHOT_MIN_BLOCKS
+#define RP_TWOSHOT_MIN_BLOCKS 2
+#endif
+constexpr int kTwoshotMinBlocks = RP_TWOSHOT_MIN_BLOCKS;
 
 __device__ __forceinline__ bool aligned16(const void* p) { return (((uintptr_t)p) & 15u) == 0; }
 
@@ -215,7 +222,7 @@ __device__ __forceinline__ void dyn_finish(const CollArgs& a, int rank, int phas
 // entered the call (the peer's previous use of its pool is complete).
 // ---------------------------------------------------------------------------
 template <int DT, int OP, int NR, bool PUSH>
-__global__ void __launch_bounds__(kThreads) ar_twoshot_dyn(const CollArgs a) {
+__global__ void __launch_bounds__(kThreads, kTwoshotMinBlocks) ar_twoshot_dyn(const CollArgs a) {
   using T = typename DType<DT>::T;
   using A = typename DType<DT>::Acc;
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;

@@ -646,6 +646,29 @@ def body_overlap(rank, world):
         assert all(torch.equal(t, gl[0]) for t in gl), "replicas diverged"
 
 
+def body_host_pipeline(rank, world):
+    """Communicator.all_reduce_host: pinned host in, pinned host out, chunked through
+    pool slots (many chunks, ragged tail, ring reuse); bit-exact vs the oracle fold,
+    and with NVLS slots within the ordering tolerance."""
+    from oracle import collectives as O
+    from paper_1902_00465_b200.comm import Communicator
+
+    comm = Communicator(device=rank, pool_bytes=64 << 20)
+    count = 5 * 8192 + 77
+    xs = _inputs(world, count, seed=321)
+    hin = torch.from_numpy(xs[rank]).pin_memory()
+    for kind, fold in (("sum", O.fold_sum), ("premean", O.fold_premean)):
+        for _ in range(2):
+            out = comm.all_reduce_host(hin, kind, chunk_bytes=8192 * 4)
+            assert out.numpy().tobytes() == fold(xs).tobytes(), kind
+    comm.enable_nvls(16 << 20)
+    out = comm.all_reduce_host(hin, "sum", chunk_bytes=1 << 20, nvls=True)
+    want = np.sum(np.stack(xs).astype(np.float64), axis=0)
+    assert np.linalg.norm(out.numpy() - want) / np.linalg.norm(want) <= 1e-6
+    comm.check()
+    comm.close()
+
+
 def _nullcontext():
     import contextlib
     return contextlib.nullcontext()
@@ -699,3 +722,7 @@ def test_dead_rank_times_out():
 
 def test_overlapped_wrap_optimizer_multiprocess():
     run_world("body_overlap")
+
+
+def test_host_pipelined_all_reduce_multiprocess():
+    run_world("body_host_pipeline")

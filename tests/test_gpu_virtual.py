@@ -584,3 +584,27 @@ def test_ragged_all_gather_and_driver_values_virtual():
         repl.run(lambda x: repl.all_gather(x, ragged=True),
                  lambda r: torch.zeros((2, 2 + (r == 1)), device=DEV))
     repl.comm.close()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("kind", ["sum", "premean", "max"])
+def test_all_reduce_host_pipelined_matches_oracle(kind, pinned):
+    """all_reduce_host: host tensors in, host tensor out through the chunked ring
+    (several chunks, a ragged tail, ring slots reused); bit-identical to the oracle's
+    rank-ordered fold, like the whole-message device call."""
+    comm = vcomm(4)
+    count = 3 * 4096 + 123  # 4 chunks of 4096 elements + a tail
+    rng = np.random.default_rng(11)
+    xs = [rng.standard_normal(count).astype(np.float32) for _ in range(4)]
+    hin = [torch.from_numpy(x) for x in xs]
+    if pinned:
+        hin = [h.pin_memory() for h in hin]
+    want = {"sum": O.fold_sum, "premean": O.fold_premean, "max": O.fold_max}[kind](xs)
+    for _ in range(2):  # second call reuses the ring
+        out = comm.all_reduce_host(hin, kind, chunk_bytes=4096 * 4)
+        assert out.numpy().tobytes() == want.tobytes()
+    f64 = [rng.standard_normal(1000) for _ in range(4)]
+    out = comm.all_reduce_host([torch.from_numpy(x) for x in f64], "sum", chunk_bytes=256 * 8)
+    assert out.numpy().tobytes() == O.fold_sum(f64).tobytes()
+    with pytest.raises(errors.ShapeError):
+        comm.all_reduce_host(hin[:3], kind)
