@@ -11,11 +11,14 @@ namespace rp {
 
 constexpr int kThreads = 512;
 constexpr int kUnroll = 2;
-// two resident 512-thread blocks per SM (<= 64 registers): 32 warps of loads in
-// flight instead of 16 (ncu: 1 block/SM at 68-84 registers, 25% occupancy,
-// long-scoreboard bound; profiles/r01_ncu_ar_twoshot_dyn_n1.txt)
+// Minimum resident blocks per SM for the two-shot. ncu shows 1 block/SM (68-84
+// registers, 25% occupancy, long-scoreboard bound), but forcing 2 (<= 64
+// registers, a few spills on odd rank counts) measured no better: N=1 184.7 vs
+// 183.9 us, N=2 124.8 vs 121.1 us, N=4 P2P 172.8 vs 175 us
+// (profiles/r01_twoshot_occupancy.txt) -- the tile loop keeps enough bytes in
+// flight at one block per SM.
 #ifndef RP_TWOSHOT_MIN_BLOCKS
-#define RP_TWOSHOT_MIN_BLOCKS 2
+#define RP_TWOSHOT_MIN_BLOCKS 1
 #endif
 constexpr int kTwoshotMinBlocks = RP_TWOSHOT_MIN_BLOCKS;
 
