@@ -72,6 +72,8 @@ enum {
                           broadcast: dst inside the NVLS region (16-byte multiple):
                           the root's multicast store reaches every rank (bit-exact);
                           AUTO picks it whenever dst lies in the region */
+  RP_ALGO_RELAY = 4,   /* broadcast, multi-process: pipelined tiles root -> owner ->
+                          peers over NVLink (P2P stores); AUTO above 1 MiB */
 };
 
 /* Status codes -> reference exception (errors.py). */

@@ -24,9 +24,11 @@ OPS = {"sum": SUM, "mean": MEAN, "max": MAX, "premean": PREMEAN}
 AUTO, ONESHOT, TWOSHOT = 0, 1, 2
 DIRECT, SCATTER = 1, 2
 NVLS = 3
+RELAY = 4
 # fused optimizer apply (rp_all_reduce_apply)
 OPT_SGD, OPT_ADAM, OPT_ADAMW = 0, 1, 2
-ALGOS = {"auto": AUTO, "oneshot": ONESHOT, "twoshot": TWOSHOT, "direct": DIRECT, "scatter": SCATTER, "nvls": NVLS}
+ALGOS = {"auto": AUTO, "oneshot": ONESHOT, "twoshot": TWOSHOT, "direct": DIRECT, "scatter": SCATTER, "nvls": NVLS,
+         "relay": RELAY}
 # layouts
 NHWC, NCHW = 0, 1
 # status codes -> exception classes (errors.py)

@@ -689,6 +689,20 @@ int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, si
     void* args[] = {&a, &ivec};
     return rp_launch(c, (const void*)bcast_push_kernel, dim3(blocks), dim3(kThreads), args, 0, stream);
   }
+  // large messages between processes: the pipelined relay (K4r). It lands in the
+  // dst itself when that is pool-resident (symmetric), else in staging
+  if (!c->is_virtual && W > 1 && bytes % 16 == 0 &&
+      (algo == RP_ALGO_RELAY || (algo == RP_ALGO_AUTO && bytes > ((size_t)1 << 20) &&
+                                 getenv("RP_BCAST_PULL") == nullptr))) {
+    size_t loff = 0;
+    const bool land_dst = symmetric_in_pool(c, (const void* const*)dst, bytes, &loff);
+    if (!land_dst) loff = scratch;
+    if (land_dst || scratch + pb <= scratch_end)
+      return rp_relay_bcast_launch(c, src[0], dst[0], bytes, root, land_dst, loff, stream, dyn_launch, a);
+    if (algo == RP_ALGO_RELAY) return rp_fail(RP_ERR_INVALID, "broadcast(relay): message exceeds the staging pool");
+  } else if (algo == RP_ALGO_RELAY) {
+    return rp_fail(RP_ERR_INVALID, "broadcast(relay): multi-process, 16-byte multiple sizes only");
+  }
   size_t doff = 0;
   if (in_place && symmetric_in_pool(c, (const void* const*)dst, bytes, &doff)) {
     a.copy_in = 0;

@@ -218,6 +218,7 @@ static int alloc_region(rp_comm* c, int r) {
   c->alloc[r] = base;
   c->table.sig[r] = (uint32_t*)base;
   c->table.data[r] = base + RP_SIGNAL_BYTES;
+  RP_CUDA_CHECK(cudaMemset(c->table.data[r] + c->tile_flags(), 0, RP_FLAG_BYTES));
   return RP_OK;
 }
 

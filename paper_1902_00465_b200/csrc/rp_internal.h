@@ -56,6 +56,10 @@
 // The BN records hold (sum, sumsq, count) as f64 for up to RP_BN_ROWS*256 channels.
 #define RP_BN_BYTES ((size_t)RP_BN_ROWS * 256 * 3 * 8)
 #define RP_OS_REGION ((size_t)4 << 20)
+// Per-tile ready flags of the relay broadcast (u32 epochs, zeroed at creation,
+// written only by that kernel): one per tile, at most RP_FLAG_WORDS tiles.
+#define RP_FLAG_WORDS 65536
+#define RP_FLAG_BYTES ((size_t)RP_FLAG_WORDS * 4)
 #define RP_MIN_POOL ((size_t)16 << 20)
 
 // Abort reasons written into the abort word (first writer wins).
@@ -87,8 +91,9 @@ struct rp_comm {
   size_t bn_partials_bytes = 0;
   void* nvls = nullptr;    // NvlsState (rp_nvls.cu): multicast-bound region, or NULL
   // end of the general staging window (see the layout above)
-  size_t scratch_end() const { return pool_bytes - RP_BN_BYTES - 2 * RP_OS_REGION; }
+  size_t scratch_end() const { return pool_bytes - RP_BN_BYTES - RP_FLAG_BYTES - 2 * RP_OS_REGION; }
   size_t oneshot_zone(int parity) const { return scratch_end() + (size_t)parity * RP_OS_REGION; }
+  size_t tile_flags() const { return pool_bytes - RP_BN_BYTES - RP_FLAG_BYTES; }
   size_t bn_records() const { return pool_bytes - RP_BN_BYTES; }
 };
 
@@ -178,6 +183,10 @@ bool rp_nvls_covers(rp_comm* c, const void* p, size_t bytes);
 // Algorithm rp_all_reduce runs (AUTO resolved): RP_ALGO_ONESHOT / TWOSHOT / NVLS
 int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
                        int dtype_comm, int dtype_out, int op, int algo);
+int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, bool land_in_dst,
+                          size_t land_off, cudaStream_t stream,
+                          int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t),
+                          CollArgs& a);
 int rp_nvls_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, cudaStream_t stream,
                          int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t),
                          CollArgs& a);

@@ -458,9 +458,136 @@ __global__ void __launch_bounds__(kNvlsThreads) bcast_nvls(const CollArgs a) {
   rp_trace(a, 7);
 }
 
+
+// ===========================================================================
+// K4r: pipelined relay broadcast (multi-process, large messages)
+// The message is cut into tiles; tile i belongs to non-root "owner" i mod (N-1).
+//   root : src tile -> owner's landing area (NVLink store), own dst; flag owner
+//   owner: waits for its flag, landing -> every other non-root's landing (NVLink)
+//          and its own dst; flags them
+//   other: waits for its flag, landing -> own dst
+// Every rank claims tiles in index order (per-warp claims), so a tile's chain
+// root -> owner -> others only ever waits on work of the same tile that was
+// claimed earlier -- no deadlock with any number of resident warps. The root's
+// egress carries S once, every non-root's ingress S and egress (N-2)/(N-1)*S:
+// the broadcast bound with P2P stores (no multicast protocol overhead), and the
+// tiles pipeline the two hops. Flags are per-tile epochs (this call's phase-0
+// base + 1, equal on every rank) in a region only this kernel writes, so they
+// never need resetting. One trailing rank barrier: the next call may write the
+// landing areas only after every rank has copied out of them.
+// a.write_off = landing offset (staging, or the dst itself when it is
+// pool-resident: copy_out = 0), a.read_off = flag-region offset, a.tile_v =
+// 16-byte vectors per tile.
+// ===========================================================================
+constexpr int kRelayU = 8;
+
+__device__ __forceinline__ void relay_copy(const char* s, char* const* d, int nd, size_t lo, size_t hi,
+                                           int lane) {
+  bool al = (((uintptr_t)s) & 15u) == 0;
+  for (int k = 0; k < nd; ++k) al = al && ((((uintptr_t)d[k]) & 15u) == 0);
+  if (al) {
+    for (size_t base = lo + (size_t)lane * 16; base < hi; base += (size_t)32 * 16 * kRelayU) {
+      uint4 r[kRelayU];
+#pragma unroll
+      for (int u = 0; u < kRelayU; ++u) {
+        const size_t o = base + (size_t)u * 32 * 16;
+        if (o < hi) r[u] = ld128(s + o);
+      }
+#pragma unroll
+      for (int u = 0; u < kRelayU; ++u) {
+        const size_t o = base + (size_t)u * 32 * 16;
+        if (o < hi)
+          for (int k = 0; k < nd; ++k) st128(d[k] + o, r[u]);
+      }
+    }
+  } else {  // a misaligned user pointer on this rank: bytes
+    for (size_t o = lo + lane; o < hi; o += 32) {
+      const char v = s[o];
+      for (int k = 0; k < nd; ++k) d[k][o] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) bcast_relay(const CollArgs a) {
+  const int rank = a.rank, W = a.world, root = a.root;
+  const size_t B = a.count;
+  const size_t tb = (size_t)a.tile_v * 16;
+  const uint32_t nt = (uint32_t)((B + tb - 1) / tb);
+  const int lane = threadIdx.x & 31;
+  rp_trace(a, 0);
+  const PhaseBase pb = phase_begin(a, rank);
+  const uint32_t epoch = pb.seen[0] + 1u;  // equal on every rank
+  uint32_t* myflags = (uint32_t*)(a.t.data[rank] + a.read_off);
+  const char* land = a.t.data[rank] + a.write_off;
+  char* dst = (char*)a.dst[rank];
+  const char* src = (const char*)a.src[rank];
+  bool ok = true;
+  for (uint32_t i = claim_tile(a, rank, 0); i < nt; i = claim_tile(a, rank, 0)) {
+    const size_t lo = (size_t)i * tb, hi = std::min(lo + tb, B);
+    const int o = (int)(i % (uint32_t)(W - 1));
+    const int owner = o < root ? o : o + 1;
+    char* d[RP_MAX_RANKS];
+    int nd = 0;
+    if (rank == root) {
+      d[nd++] = a.t.data[owner] + a.write_off;
+      if (dst != src) d[nd++] = dst;
+      relay_copy(src, d, nd, lo, hi, lane);
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        st_relaxed_sys((uint32_t*)(a.t.data[owner] + a.read_off) + i, epoch);
+      }
+      continue;
+    }
+    // lane 0 spins (one poller per warp), then every lane acquires the flag once
+    if (lane == 0) ok = wait_reach(a.t, a.world, a.timeout_ns, rank, myflags + i, epoch);
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) break;
+    (void)ld_acquire_sys(myflags + i);
+    if (rank == owner) {
+      for (int q = 0; q < W; ++q)
+        if (q != root && q != rank) d[nd++] = a.t.data[q] + a.write_off;
+    }
+    if (a.copy_out) d[nd++] = dst;
+    if (nd) relay_copy(land, d, nd, lo, hi, lane);
+    if (rank == owner && W > 2) {
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int q = 0; q < W; ++q)
+          if (q != root && q != rank) st_relaxed_sys((uint32_t*)(a.t.data[q] + a.read_off) + i, epoch);
+      }
+    }
+  }
+  if (!ok) return;  // the abort word is set: every rank leaves its waits
+  if (!phase_end(a, rank, 0, pb)) return;
+  dyn_finish(a, rank, 1, pb);
+  rp_trace(a, 7);
+}
+
 }  // namespace rp
 
 using namespace rp;
+
+int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, bool land_in_dst,
+                          size_t land_off, cudaStream_t stream,
+                          int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t),
+                          CollArgs& a) {
+  if (bytes % 16) return rp_fail(RP_ERR_INVALID, "broadcast(relay): bytes must be a multiple of 16");
+  const size_t V = bytes / 16;
+  size_t tv = std::max<size_t>(256, (V + RP_FLAG_WORDS - 1) / RP_FLAG_WORDS);  // >= 4 KiB tiles
+  tv = (tv + 31) / 32 * 32;
+  a.count = bytes;
+  a.root = root;
+  a.chunk = V;
+  a.src[c->rank] = src;
+  a.dst[c->rank] = dst;
+  a.write_off = land_off;
+  a.read_off = c->tile_flags();
+  a.copy_in = 0;
+  a.copy_out = land_in_dst ? 0 : 1;
+  return dyn(c, (const void*)bcast_relay, a, stream, "bcast_relay", 0, kThreads, (uint32_t)tv);
+}
 
 int rp_nvls_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, cudaStream_t stream,
                          int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t),

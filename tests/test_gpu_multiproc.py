@@ -127,7 +127,7 @@ def body_gather_broadcast(rank, world):
         comm.all_gather_tensor(out[rank], out=out)
         assert out.cpu().numpy().tobytes() == np.concatenate(xs).tobytes(), count
         for root in range(world):
-            for algo in ("auto", "direct", "scatter"):
+            for algo in ("auto", "direct", "scatter") + (("relay",) if count % 4 == 0 else ()):
                 x = torch.from_numpy(xs[rank]).to(dev)
                 comm.broadcast_tensor(x, root=root, algo=algo)
                 assert x.cpu().numpy().tobytes() == xs[root].tobytes(), (count, root, algo)
@@ -669,6 +669,43 @@ def body_host_pipeline(rank, world):
     comm.close()
 
 
+def body_relay_broadcast(rank, world):
+    """Pipelined relay broadcast (K4r): bit-exact for every root, landing in staging
+    (user dst, aligned or not) or straight in a pool-resident dst, many tiles,
+    repeated calls (per-tile epoch flags are never reset)."""
+    from paper_1902_00465_b200.comm import Communicator
+
+    dev = torch.device(f"cuda:{rank}")
+    comm = Communicator(device=rank, pool_bytes=96 << 20)
+    for nbytes in (16, (1 << 20) + 16, (9 << 20) + 4096):
+        want = {r: np.random.default_rng(nbytes + r).integers(0, 256, nbytes + 1, dtype=np.uint8)
+                for r in range(world)}
+        pool_dst = comm.alloc(nbytes, torch.uint8)
+        for root in range(world):
+            src = torch.from_numpy(want[root]).to(dev)
+            for mode in ("user", "misaligned", "pool", "pool_in_place"):
+                if mode == "user":
+                    out = torch.full((nbytes,), rank + 1, dtype=torch.uint8, device=dev)
+                    comm.broadcast_tensor(src[:nbytes], root=root, out=out, algo="relay")
+                elif mode == "misaligned":
+                    big = torch.full((nbytes + 1,), rank + 1, dtype=torch.uint8, device=dev)
+                    out = big[1:]
+                    comm.broadcast_tensor(src[:nbytes], root=root, out=out, algo="relay")
+                elif mode == "pool":
+                    out = pool_dst
+                    out.fill_(rank + 3)
+                    comm.broadcast_tensor(src[:nbytes], root=root, out=out, algo="relay")
+                else:
+                    out = pool_dst
+                    out.fill_(rank + 5)
+                    if rank == root:
+                        out.copy_(src[:nbytes])
+                    comm.broadcast_tensor(out, root=root, algo="relay")
+                assert np.array_equal(out.cpu().numpy(), want[root][:nbytes]), (nbytes, root, mode)
+    comm.check()
+    comm.close()
+
+
 def _nullcontext():
     import contextlib
     return contextlib.nullcontext()
@@ -726,3 +763,7 @@ def test_overlapped_wrap_optimizer_multiprocess():
 
 def test_host_pipelined_all_reduce_multiprocess():
     run_world("body_host_pipeline")
+
+
+def test_relay_broadcast_multiprocess():
+    run_world("body_relay_broadcast")

@@ -75,6 +75,8 @@ def main():
                                                                 else ["auto"])
         if "nccl" in a.algos.split(",") and op != "all_reduce":
             algos = algos + ["nccl"]  # comparison column only: NCCL is never on the product path
+        if op == "broadcast" and world > 1:
+            algos = algos + ["relay"]  # pipelined P2P relay (K4r); AUTO's choice above 1 MiB
         if "nvls" in a.algos.split(",") and op == "broadcast":
             algos = algos + ["nvls"]  # in place in the NVLS region: the root's multicast store
         for lg in range(a.min_log2, a.max_log2 + 1):
@@ -123,6 +125,8 @@ def main():
                         fn = lambda: comm.broadcast_tensor(nvls_buf[:count], root=0)  # noqa: E731
                     elif world == 1:
                         fn = lambda: comm.broadcast(xs, root=0, outs=os_, algo=algo)  # noqa: E731
+                    elif algo == "relay" and size % 16:
+                        continue
                     else:
                         fn = lambda: comm.broadcast_tensor(xs[0], root=0, out=os_[0], algo=algo)  # noqa: E731
                     factor = 1.0
