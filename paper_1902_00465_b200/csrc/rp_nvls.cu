@@ -481,87 +481,109 @@ __global__ void __launch_bounds__(kNvlsThreads) bcast_nvls(const CollArgs a) {
 // ===========================================================================
 constexpr int kRelayU = 8;
 
-__device__ __forceinline__ void relay_copy(const char* s, char* const* d, int nd, size_t lo, size_t hi,
-                                           int lane) {
+// Block-wide copy of bytes [lo, hi) from s to nd destinations (16-byte vectors,
+// kRelayU in flight per thread; bytes when a pointer is misaligned).
+__device__ __forceinline__ void relay_copy(const char* s, char* const* d, int nd, size_t lo, size_t hi) {
   bool al = (((uintptr_t)s) & 15u) == 0;
   for (int k = 0; k < nd; ++k) al = al && ((((uintptr_t)d[k]) & 15u) == 0);
   if (al) {
-    for (size_t base = lo + (size_t)lane * 16; base < hi; base += (size_t)32 * 16 * kRelayU) {
+    const size_t step = (size_t)blockDim.x * 16 * kRelayU;
+    for (size_t base = lo + (size_t)threadIdx.x * 16; base < hi; base += step) {
       uint4 r[kRelayU];
 #pragma unroll
       for (int u = 0; u < kRelayU; ++u) {
-        const size_t o = base + (size_t)u * 32 * 16;
+        const size_t o = base + (size_t)u * blockDim.x * 16;
         if (o < hi) r[u] = ld128(s + o);
       }
 #pragma unroll
       for (int u = 0; u < kRelayU; ++u) {
-        const size_t o = base + (size_t)u * 32 * 16;
+        const size_t o = base + (size_t)u * blockDim.x * 16;
         if (o < hi)
           for (int k = 0; k < nd; ++k) st128(d[k] + o, r[u]);
       }
     }
   } else {  // a misaligned user pointer on this rank: bytes
-    for (size_t o = lo + lane; o < hi; o += 32) {
+    for (size_t o = lo + threadIdx.x; o < hi; o += blockDim.x) {
       const char v = s[o];
       for (int k = 0; k < nd; ++k) d[k][o] = v;
     }
   }
 }
 
+// Publish this block's tile: every thread's stores happen-before thread 0's
+// system fence (bar.sync orders them), then the flag stores.
+__device__ __forceinline__ void relay_publish(const CollArgs& a, const int* q, int nq, uint32_t i, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int k = 0; k < nq; ++k) st_relaxed_sys((uint32_t*)(a.t.data[q[k]] + a.read_off) + i, epoch);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) bcast_relay(const CollArgs a) {
+  __shared__ uint32_t s_tile;
+  __shared__ int s_ok;
   const int rank = a.rank, W = a.world, root = a.root;
   const size_t B = a.count;
   const size_t tb = (size_t)a.tile_v * 16;
   const uint32_t nt = (uint32_t)((B + tb - 1) / tb);
-  const int lane = threadIdx.x & 31;
   rp_trace(a, 0);
   const PhaseBase pb = phase_begin(a, rank);
-  const uint32_t epoch = pb.seen[0] + 1u;  // equal on every rank
+  // landing straight in a pool-resident dst: every receiver must have entered the
+  // call (its earlier writes to dst are done) before anyone stores into it
+  if (a.copy_in && !phase_end(a, rank, 0, pb)) return;
+  const uint32_t epoch = pb.seen[1] + 1u;  // equal on every rank
   uint32_t* myflags = (uint32_t*)(a.t.data[rank] + a.read_off);
   const char* land = a.t.data[rank] + a.write_off;
   char* dst = (char*)a.dst[rank];
   const char* src = (const char*)a.src[rank];
-  bool ok = true;
-  for (uint32_t i = claim_tile(a, rank, 0); i < nt; i = claim_tile(a, rank, 0)) {
+  if (threadIdx.x == 0) s_ok = 1;
+  for (;;) {
+    // one tile per block at a time, claimed in index order
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + 1, 1u);
+    __syncthreads();
+    const uint32_t i = s_tile;
+    if (i >= nt || !s_ok) break;
     const size_t lo = (size_t)i * tb, hi = std::min(lo + tb, B);
     const int o = (int)(i % (uint32_t)(W - 1));
     const int owner = o < root ? o : o + 1;
     char* d[RP_MAX_RANKS];
-    int nd = 0;
+    int q[RP_MAX_RANKS];
+    int nd = 0, nq = 0;
     if (rank == root) {
       d[nd++] = a.t.data[owner] + a.write_off;
       if (dst != src) d[nd++] = dst;
-      relay_copy(src, d, nd, lo, hi, lane);
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-        st_relaxed_sys((uint32_t*)(a.t.data[owner] + a.read_off) + i, epoch);
-      }
+      relay_copy(src, d, nd, lo, hi);
+      q[nq++] = owner;
+      relay_publish(a, q, nq, i, epoch);
       continue;
     }
-    // lane 0 spins (one poller per warp), then every lane acquires the flag once
-    if (lane == 0) ok = wait_reach(a.t, a.world, a.timeout_ns, rank, myflags + i, epoch);
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (!ok) break;
-    (void)ld_acquire_sys(myflags + i);
+    if (threadIdx.x == 0 && !wait_reach(a.t, a.world, a.timeout_ns, rank, myflags + i, epoch)) s_ok = 0;
+    __syncthreads();
+    if (!s_ok) break;
+    (void)ld_acquire_sys(myflags + i);  // every thread acquires the published tile
     if (rank == owner) {
-      for (int q = 0; q < W; ++q)
-        if (q != root && q != rank) d[nd++] = a.t.data[q] + a.write_off;
+      for (int p = 0; p < W; ++p)
+        if (p != root && p != rank) {
+          d[nd++] = a.t.data[p] + a.write_off;
+          q[nq++] = p;
+        }
     }
     if (a.copy_out) d[nd++] = dst;
-    if (nd) relay_copy(land, d, nd, lo, hi, lane);
-    if (rank == owner && W > 2) {
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-        for (int q = 0; q < W; ++q)
-          if (q != root && q != rank) st_relaxed_sys((uint32_t*)(a.t.data[q] + a.read_off) + i, epoch);
-      }
+    if (nd) relay_copy(land, d, nd, lo, hi);
+    if (nq) relay_publish(a, q, nq, i, epoch);
+  }
+  if (!s_ok) return;  // the abort word is set: every rank leaves its waits
+  if (!phase_end(a, rank, 1, pb)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // dyn_finish for the phases this call used
+    if (a.copy_in) state_store(a.t, rank, RP_ST_PH_SEEN + 0, pb.seen[0] + 1u);
+    state_store(a.t, rank, RP_ST_PH_SEEN + 1, pb.seen[1] + 1u);
+    for (int k = 0; k < 3; ++k) {
+      state_store(a.t, rank, RP_CTR_ROW * RP_MAX_RANKS + k, 0u);
+      state_store(a.t, rank, RP_CTR_ROW * RP_MAX_RANKS + 4 + k, 0u);
     }
   }
-  if (!ok) return;  // the abort word is set: every rank leaves its waits
-  if (!phase_end(a, rank, 0, pb)) return;
-  dyn_finish(a, rank, 1, pb);
   rp_trace(a, 7);
 }
 
@@ -575,8 +597,9 @@ int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, 
                           CollArgs& a) {
   if (bytes % 16) return rp_fail(RP_ERR_INVALID, "broadcast(relay): bytes must be a multiple of 16");
   const size_t V = bytes / 16;
-  size_t tv = std::max<size_t>(256, (V + RP_FLAG_WORDS - 1) / RP_FLAG_WORDS);  // >= 4 KiB tiles
-  tv = (tv + 31) / 32 * 32;
+  // one 64 KiB tile per block at a time (one system fence per 64 KiB published)
+  size_t tv = std::max<size_t>(4096, (V + RP_FLAG_WORDS - 1) / RP_FLAG_WORDS);
+  tv = (tv + 511) / 512 * 512;
   a.count = bytes;
   a.root = root;
   a.chunk = V;
@@ -584,7 +607,7 @@ int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, 
   a.dst[c->rank] = dst;
   a.write_off = land_off;
   a.read_off = c->tile_flags();
-  a.copy_in = 0;
+  a.copy_in = land_in_dst ? 1 : 0;  // entry barrier (see the kernel)
   a.copy_out = land_in_dst ? 0 : 1;
   return dyn(c, (const void*)bcast_relay, a, stream, "bcast_relay", 0, kThreads, (uint32_t)tv);
 }
