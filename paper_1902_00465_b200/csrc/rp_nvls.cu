@@ -9,6 +9,9 @@
 // Bootstrap: the multicast handle is a POSIX file descriptor (fabric handles are
 // not permitted on this pool, tools/mc_probe.cu), handed from rank 0 to its peers
 // over an abstract-namespace Unix socket with SCM_RIGHTS.
+//
+// Also here, as the other dynamically scheduled broadcasts: the NVLS broadcast
+// (K4n, multicast store) and the pipelined P2P relay broadcast (K4r).
 #include <cuda.h>
 #include <string.h>
 #include <sys/socket.h>
@@ -479,10 +482,9 @@ __global__ void __launch_bounds__(kNvlsThreads) bcast_nvls(const CollArgs a) {
 // pool-resident: copy_out = 0), a.read_off = flag-region offset, a.tile_v =
 // 16-byte vectors per tile.
 // ===========================================================================
-constexpr int kRelayU = 8;
-
 // Block-wide copy of bytes [lo, hi) from s to nd destinations (16-byte vectors,
 // kRelayU in flight per thread; bytes when a pointer is misaligned).
+template <int kRelayU>
 __device__ __forceinline__ void relay_copy(const char* s, char* const* d, int nd, size_t lo, size_t hi) {
   bool al = (((uintptr_t)s) & 15u) == 0;
   for (int k = 0; k < nd; ++k) al = al && ((((uintptr_t)d[k]) & 15u) == 0);
@@ -520,7 +522,9 @@ __device__ __forceinline__ void relay_publish(const CollArgs& a, const int* q, i
   }
 }
 
-__global__ void __launch_bounds__(kThreads) bcast_relay(const CollArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) bcast_relay(const CollArgs a) {
+  constexpr int kU = MINB > 1 ? 4 : 8;  // 16-byte vectors in flight per thread
   __shared__ uint32_t s_tile;
   __shared__ int s_ok;
   const int rank = a.rank, W = a.world, root = a.root;
@@ -554,7 +558,7 @@ __global__ void __launch_bounds__(kThreads) bcast_relay(const CollArgs a) {
     if (rank == root) {
       d[nd++] = a.t.data[owner] + a.write_off;
       if (dst != src) d[nd++] = dst;
-      relay_copy(src, d, nd, lo, hi);
+      relay_copy<kU>(src, d, nd, lo, hi);
       q[nq++] = owner;
       relay_publish(a, q, nq, i, epoch);
       continue;
@@ -571,7 +575,7 @@ __global__ void __launch_bounds__(kThreads) bcast_relay(const CollArgs a) {
         }
     }
     if (a.copy_out) d[nd++] = dst;
-    if (nd) relay_copy(land, d, nd, lo, hi);
+    if (nd) relay_copy<kU>(land, d, nd, lo, hi);
     if (nq) relay_publish(a, q, nq, i, epoch);
   }
   if (!s_ok) return;  // the abort word is set: every rank leaves its waits
@@ -597,8 +601,11 @@ int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, 
                           CollArgs& a) {
   if (bytes % 16) return rp_fail(RP_ERR_INVALID, "broadcast(relay): bytes must be a multiple of 16");
   const size_t V = bytes / 16;
-  // one 64 KiB tile per block at a time (one system fence per 64 KiB published)
-  size_t tv = std::max<size_t>(4096, (V + RP_FLAG_WORDS - 1) / RP_FLAG_WORDS);
+  // one tile per block at a time (one system fence per tile published); 64 KiB
+  // by default, RP_RELAY_TILE_KB overrides (A/B)
+  size_t tmin = 4096;
+  if (const char* e = getenv("RP_RELAY_TILE_KB")) tmin = std::max<size_t>(512, (size_t)atoi(e) * 64);
+  size_t tv = std::max<size_t>(tmin, (V + RP_FLAG_WORDS - 1) / RP_FLAG_WORDS);
   tv = (tv + 511) / 512 * 512;
   a.count = bytes;
   a.root = root;
@@ -609,7 +616,9 @@ int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, 
   a.read_off = c->tile_flags();
   a.copy_in = land_in_dst ? 1 : 0;  // entry barrier (see the kernel)
   a.copy_out = land_in_dst ? 0 : 1;
-  return dyn(c, (const void*)bcast_relay, a, stream, "bcast_relay", 0, kThreads, (uint32_t)tv);
+  const char* occ = getenv("RP_RELAY_OCC");
+  const void* fn = (occ && occ[0] == '1') ? (const void*)bcast_relay<1> : (const void*)bcast_relay<2>;
+  return dyn(c, fn, a, stream, "bcast_relay", 0, kThreads, (uint32_t)tv);
 }
 
 int rp_nvls_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, cudaStream_t stream,
