@@ -522,11 +522,35 @@ __device__ __forceinline__ void relay_publish(const CollArgs& a, const int* q, i
   }
 }
 
+// Claim the next tile index of `counter` (one atomic per block, index order).
+__device__ __forceinline__ uint32_t relay_claim(const CollArgs& a, int rank, int counter) {
+  __shared__ uint32_t s_tile;
+  __syncthreads();
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + counter, 1u);
+  __syncthreads();
+  return s_tile;
+}
+
+// Block-wide wait for tile i's flag (thread 0 spins; every thread then acquires it).
+__device__ __forceinline__ bool relay_wait(const CollArgs& a, int rank, const uint32_t* f, uint32_t epoch) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = wait_reach(a.t, a.world, a.timeout_ns, rank, f, epoch) ? 1 : 0;
+  __syncthreads();
+  if (!s_ok) return false;
+  (void)ld_acquire_sys(f);
+  return true;
+}
+
+// Roles: the root pushes every tile (claim counter 1). A non-root's blocks split:
+// even blocks FORWARD the tiles it owns (wait for the root's flag, store to the
+// other non-roots and its own dst, publish) on counter 1, odd blocks RECEIVE the
+// tiles others own (wait for the owner's flag, copy the landing area to dst) on
+// counter 2. Forwarding never waits on receiving, so blocks parked on flags never
+// starve the relays (one role for every block left them ~1/(N-1) of the SMs).
+// Landing in a pool-resident dst there is nothing to receive: all blocks forward.
 template <int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) bcast_relay(const CollArgs a) {
   constexpr int kU = MINB > 1 ? 4 : 8;  // 16-byte vectors in flight per thread
-  __shared__ uint32_t s_tile;
-  __shared__ int s_ok;
   const int rank = a.rank, W = a.world, root = a.root;
   const size_t B = a.count;
   const size_t tb = (size_t)a.tile_v * 16;
@@ -541,44 +565,57 @@ __global__ void __launch_bounds__(kThreads, MINB) bcast_relay(const CollArgs a) 
   const char* land = a.t.data[rank] + a.write_off;
   char* dst = (char*)a.dst[rank];
   const char* src = (const char*)a.src[rank];
-  if (threadIdx.x == 0) s_ok = 1;
-  for (;;) {
-    // one tile per block at a time, claimed in index order
-    __syncthreads();
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.t.sig[rank] + (size_t)RP_CTR_ROW * RP_MAX_RANKS + 1, 1u);
-    __syncthreads();
-    const uint32_t i = s_tile;
-    if (i >= nt || !s_ok) break;
-    const size_t lo = (size_t)i * tb, hi = std::min(lo + tb, B);
-    const int o = (int)(i % (uint32_t)(W - 1));
-    const int owner = o < root ? o : o + 1;
-    char* d[RP_MAX_RANKS];
-    int q[RP_MAX_RANKS];
-    int nd = 0, nq = 0;
-    if (rank == root) {
-      d[nd++] = a.t.data[owner] + a.write_off;
-      if (dst != src) d[nd++] = dst;
-      relay_copy<kU>(src, d, nd, lo, hi);
-      q[nq++] = owner;
-      relay_publish(a, q, nq, i, epoch);
-      continue;
-    }
-    if (threadIdx.x == 0 && !wait_reach(a.t, a.world, a.timeout_ns, rank, myflags + i, epoch)) s_ok = 0;
-    __syncthreads();
-    if (!s_ok) break;
-    (void)ld_acquire_sys(myflags + i);  // every thread acquires the published tile
-    if (rank == owner) {
+  const uint32_t W1 = (uint32_t)(W - 1);
+  const int me = rank < root ? rank : rank - 1;  // this non-root's owner index
+  const bool split = rank != root && a.copy_out && W > 2 && gridDim.x > 1;
+  const bool fwd = !split || (blockIdx.x & 1) == 0;
+  const bool recv = rank != root && a.copy_out && W > 2 && (!split || (blockIdx.x & 1) == 1);
+  bool ok = true;
+  char* d[RP_MAX_RANKS];
+  int q[RP_MAX_RANKS];
+  if (fwd) {
+    for (uint32_t k = relay_claim(a, rank, 1);; k = relay_claim(a, rank, 1)) {
+      int nd = 0, nq = 0;
+      if (rank == root) {
+        const uint32_t i = k;
+        if (i >= nt) break;
+        const size_t lo = (size_t)i * tb, hi = std::min(lo + tb, B);
+        const int o = (int)(i % W1);
+        const int owner = o < root ? o : o + 1;
+        d[nd++] = a.t.data[owner] + a.write_off;
+        if (dst != src) d[nd++] = dst;
+        relay_copy<kU>(src, d, nd, lo, hi);
+        q[nq++] = owner;
+        relay_publish(a, q, nq, i, epoch);
+        continue;
+      }
+      const uint32_t i = (uint32_t)me + k * W1;  // the k-th tile this rank owns
+      if (i >= nt) break;
+      const size_t lo = (size_t)i * tb, hi = std::min(lo + tb, B);
+      if (!(ok = relay_wait(a, rank, myflags + i, epoch))) break;
       for (int p = 0; p < W; ++p)
         if (p != root && p != rank) {
           d[nd++] = a.t.data[p] + a.write_off;
           q[nq++] = p;
         }
+      if (a.copy_out) d[nd++] = dst;
+      if (nd) relay_copy<kU>(land, d, nd, lo, hi);
+      if (nq) relay_publish(a, q, nq, i, epoch);
     }
-    if (a.copy_out) d[nd++] = dst;
-    if (nd) relay_copy<kU>(land, d, nd, lo, hi);
-    if (nq) relay_publish(a, q, nq, i, epoch);
   }
-  if (!s_ok) return;  // the abort word is set: every rank leaves its waits
+  if (recv && ok) {
+    const uint32_t W2 = (uint32_t)(W - 2);
+    for (uint32_t j = relay_claim(a, rank, 2);; j = relay_claim(a, rank, 2)) {
+      const uint32_t r = j % W2;
+      const uint32_t i = (j / W2) * W1 + (r < (uint32_t)me ? r : r + 1);  // j-th tile owned by others
+      if (i >= nt) break;
+      const size_t lo = (size_t)i * tb, hi = std::min(lo + tb, B);
+      if (!(ok = relay_wait(a, rank, myflags + i, epoch))) break;
+      d[0] = dst;
+      relay_copy<kU>(land, d, 1, lo, hi);
+    }
+  }
+  if (!ok) return;  // the abort word is set: every rank leaves its waits
   if (!phase_end(a, rank, 1, pb)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // dyn_finish for the phases this call used
     if (a.copy_in) state_store(a.t, rank, RP_ST_PH_SEEN + 0, pb.seen[0] + 1u);
@@ -617,6 +654,8 @@ int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, 
   a.copy_in = land_in_dst ? 1 : 0;  // entry barrier (see the kernel)
   a.copy_out = land_in_dst ? 0 : 1;
   const char* occ = getenv("RP_RELAY_OCC");
+  // 2 blocks per SM (4 vectors in flight per thread) measured best: N=4 256 MiB
+  // 432 vs 539 us at 1 block per SM (profiles/r01_relay_ab.txt)
   const void* fn = (occ && occ[0] == '1') ? (const void*)bcast_relay<1> : (const void*)bcast_relay<2>;
   return dyn(c, fn, a, stream, "bcast_relay", 0, kThreads, (uint32_t)tv);
 }
