@@ -323,6 +323,7 @@ int dyn_launch(rp_comm* c, const void* fn, CollArgs& a, cudaStream_t stream, con
 void base_args(rp_comm* c, CollArgs& a) {
   a.trace = nullptr;
   a.tile_v = 0;
+  a.relay_root_blocks = 0;
   a.t = c->table;
   a.world = c->world;
   a.rank = c->is_virtual ? -1 : c->rank;

@@ -125,6 +125,7 @@ struct CollArgs {
   uint64_t timeout_ns;
   unsigned long long* trace;  // RP_TRACE analysis: per-block %globaltimer stamps, or NULL
   uint32_t tile_v;            // dynamically scheduled kernels: vectors (16 B) per tile
+  int relay_root_blocks;      // relay broadcast: blocks the root pushes with
 };
 
 // error plumbing
