@@ -568,10 +568,12 @@ __global__ void __launch_bounds__(kThreads, MINB) bcast_relay(const CollArgs a) 
   const uint32_t W1 = (uint32_t)(W - 1);
   const int me = rank < root ? rank : rank - 1;  // this non-root's owner index
   const bool split = rank != root && a.copy_out && W > 2 && gridDim.x > 1;
-  // the root keeps only a.root_blocks blocks pushing: enough bytes in flight for
-  // the link, few enough tiles in progress that they complete (and the owners'
-  // relays start) early -- every root block holding a tile delays the first one
-  const bool fwd = rank == root ? (int)blockIdx.x < a.relay_root_blocks : (!split || (blockIdx.x & 1) == 0);
+  // a.relay_root_blocks > 0 caps the blocks the root pushes with (A/B knob: fewer
+  // tiles in progress start the relays earlier, but each SM's NVLink stores
+  // sustain only ~5 GB/s, so the root needs every block -- 64 blocks: 786 vs 433 us
+  // at 256 MiB, N=4; profiles/r01_relay_ab.txt)
+  const bool fwd = rank == root ? (a.relay_root_blocks <= 0 || (int)blockIdx.x < a.relay_root_blocks)
+                                : (!split || (blockIdx.x & 1) == 0);
   const bool recv = rank != root && a.copy_out && W > 2 && (!split || (blockIdx.x & 1) == 1);
   bool ok = true;
   char* d[RP_MAX_RANKS];
@@ -655,8 +657,8 @@ int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, 
   a.write_off = land_off;
   a.read_off = c->tile_flags();
   a.copy_in = land_in_dst ? 1 : 0;  // entry barrier (see the kernel)
-  a.relay_root_blocks = 64;
-  if (const char* e = getenv("RP_RELAY_ROOT_BLOCKS")) a.relay_root_blocks = std::max(1, atoi(e));
+  a.relay_root_blocks = 0;  // all
+  if (const char* e = getenv("RP_RELAY_ROOT_BLOCKS")) a.relay_root_blocks = std::max(0, atoi(e));
   a.copy_out = land_in_dst ? 0 : 1;
   const char* occ = getenv("RP_RELAY_OCC");
   // 2 blocks per SM (4 vectors in flight per thread) measured best: N=4 256 MiB
