@@ -347,6 +347,29 @@ def run_ours(args, rank, world, local):
     return line
 
 
+def bind_host_to_gpu(local: int) -> str:
+    """Restrict this process to the CPU cores NVML reports as local to its GPU, so
+    the pinned host buffers of the e2e path are first-touched on the GPU's NUMA
+    node (the host side of every H2D / D2H copy). Returns what was done."""
+    try:
+        import pynvml
+        import torch
+
+        pr = torch.cuda.get_device_properties(local)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        ncpu = os.cpu_count() or 1
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = [c for c in range(ncpu) if (mask[c // 64] >> (c % 64)) & 1]
+        cpus = [c for c in cpus if c in os.sched_getaffinity(0)]
+        if not cpus:
+            return "unbound (no local cores in this process's affinity)"
+        os.sched_setaffinity(0, cpus)
+        return f"bound to the GPU's {len(cpus)} NVML-local cores"
+    except Exception as e:  # no NVML / affinity support: leave the process as it is
+        return f"unbound ({type(e).__name__})"
+
+
 def run_e2e(args, comm, world, n, count, dev, stream):
     """The same metric through the public host-buffer API: pinned host tensors in,
     pinned host tensor out (Communicator / VirtualCommunicator.all_reduce_host,
@@ -356,6 +379,7 @@ def run_e2e(args, comm, world, n, count, dev, stream):
 
     k = max(1, args.e2e_steps)
     reps = n if world == 1 else 1
+    numa = bind_host_to_gpu(dev.index if dev.index is not None else 0)
     host_in = [torch.randn(count).pin_memory() for _ in range(reps)]
     host_out = torch.empty(count).pin_memory()
     nvls = bool(getattr(args, "use_nvls", False))
@@ -377,7 +401,8 @@ def run_e2e(args, comm, world, n, count, dev, stream):
     return {"value": busbw(args.bytes, n, ms / 1e3) * world, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": reps * count * 4, "d2h_bytes_per_step": count * 4,
             "path": "pinned host -> all_reduce_host (chunks: cudaMemcpyAsync H2D | rp_all_reduce(_v) in place "
-                    "in pool slots | D2H, overlapped) -> pinned host" + (" [NVLS slots]" if nvls else "")}
+                    "in pool slots | D2H, overlapped) -> pinned host" + (" [NVLS slots]" if nvls else ""),
+            "host": numa}
 
 
 def main():

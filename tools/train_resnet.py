@@ -46,6 +46,8 @@ def main():
     p.add_argument("--overlap-blocks", type=int, default=None, help="grid cap of overlapped exchanges (0: none)")
     p.add_argument("--no-grad-views", action="store_true", help="pack/unpack gradients instead of bucket views")
     p.add_argument("--overlap-priority", type=int, default=-1, help="side-stream priority (-1 high, 0 normal)")
+    p.add_argument("--overlap-dry-kernel", action="store_true",
+                   help="diagnostic: like --overlap-dry, plus one tiny kernel per bucket on the side stream")
     p.add_argument("--overlap-dry", action="store_true",
                    help="diagnostic: hooks and bucket bookkeeping only, no exchange (measures the hook overhead)")
     a = p.parse_args()
@@ -77,9 +79,11 @@ def main():
     net = model.local
     if a.overlap and world > 1:
         opt.stream = torch.cuda.Stream(device=dev, priority=a.overlap_priority)
-        if a.overlap_dry:
+        if a.overlap_dry or a.overlap_dry_kernel:
+            tiny = torch.zeros(1, device=dev)
             for b in opt.buckets:
-                b.reduce = lambda kind, grads=None: None
+                b.reduce = (lambda kind, grads=None, attached=False: tiny.add_(1)) if a.overlap_dry_kernel \
+                    else (lambda kind, grads=None, attached=False: None)
     if a.no_average:
         opt.average_gradients = lambda: None
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
