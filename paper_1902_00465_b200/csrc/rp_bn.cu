@@ -341,6 +341,12 @@ __device__ __forceinline__ bool bn_barrier(const ExArgs& a, int rank, int nblk, 
 
 __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk, int nblk) {
   __shared__ double red[kExThreads][2];
+  // BN calls completed so far (one barrier each, equal on every rank); the record
+  // set alternates with its parity, so the next call can write its records while a
+  // slow peer may still be reading this one's: a rank reuses a set only after the
+  // following call's barrier, which every peer reaches after its reads
+  const uint32_t seen = state_load(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE);
+  const size_t bn_off = a.bn_off + (size_t)(seen & 1u) * RP_BN_HALF;
   const int rep = a.rank >= 0 ? 0 : rank;  // local replica index
   const int tpc = kExThreads / a.cpb;      // threads per channel
   const int lane = threadIdx.x % tpc;
@@ -370,19 +376,18 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
       if (a.out2[rep]) a.out2[rep][c] = (float)s1;
       if (a.out3[rep]) a.out3[rep][c] = (float)s2;
     }
-    double* rec = (double*)(a.t.data[rank] + a.bn_off) + c * 3;
+    double* rec = (double*)(a.t.data[rank] + bn_off) + c * 3;
     rec[0] = s1;
     rec[1] = s2;
     rec[2] = a.local_count[rep];
   }
   // one rank, one replica: every thread reads back only its own records -- no barrier
   const bool sync = a.world > 1;
-  const uint32_t seen = sync ? state_load(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE) : 0u;
   if (sync && !bn_barrier(a, rank, nblk, seen + 1u)) return;
   if (lane == 0 && c < C) {
     double A1 = 0.0, A2 = 0.0, Mt = 0.0;
     for (int p = 0; p < a.world; ++p) {  // ascending rank order
-      const double* rec = (const double*)(a.t.data[p] + a.bn_off) + c * 3;
+      const double* rec = (const double*)(a.t.data[p] + bn_off) + c * 3;
       A1 += rec[0];
       A2 += rec[1];
       Mt += rec[2];
@@ -400,10 +405,9 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
     }
     if (c == 0 && a.count[rep]) *a.count[rep] = Mt;
   }
-  if (!sync) return;
-  // records are re-written by the next call: hold every rank until all have read them
-  if (!bn_barrier(a, rank, nblk, seen + 2u)) return;
-  if (blk == 0 && threadIdx.x == 0) state_store(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE, seen + 2u);
+  // advance the call count (after this block's barrier every block of this rank has
+  // read `seen`; the state is local). One rank: the count still flips the parity.
+  if (blk == 0 && threadIdx.x == 0) state_store(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE, seen + 1u);
 }
 
 __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {

@@ -54,7 +54,8 @@
 // by a trailing barrier, so a peer that already started the next call and
 // pushes without a start barrier can never clobber data still being read.
 // The BN records hold (sum, sumsq, count) as f64 for up to RP_BN_ROWS*256 channels.
-#define RP_BN_BYTES ((size_t)RP_BN_ROWS * 256 * 3 * 8)
+#define RP_BN_HALF ((size_t)RP_BN_ROWS * 256 * 3 * 8)
+#define RP_BN_BYTES (2 * RP_BN_HALF)  // two record sets, alternating by call parity
 #define RP_OS_REGION ((size_t)4 << 20)
 // Per-tile ready flags of the relay broadcast (u32 epochs, zeroed at creation,
 // written only by that kernel): one per tile, at most RP_FLAG_WORDS tiles.

@@ -57,6 +57,7 @@ def main():
     lib = _lib.load()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_sink = torch.empty((), dtype=torch.int64, device=dev)
+    align = torch.zeros(4, device=dev)
     stream = torch.cuda.current_stream(dev)
     rows_out = []
     shapes = SHAPES if a.only is None else [tuple(int(v) for v in a.only.split("x"))]
@@ -109,6 +110,8 @@ def main():
                 flush.zero_()
                 if a.flush == "write+read":
                     flush_sink.copy_(flush.view(torch.int64).sum())
+                if world > 1:  # untimed tiny collective: ranks leave the flush together
+                    comm.all_reduce_tensor(align, "sum", out=align)
                 e0.record(stream)
                 fn()
                 e1.record(stream)
