@@ -21,6 +21,10 @@ constexpr int kUnroll = 2;
 #define RP_TWOSHOT_MIN_BLOCKS 1
 #endif
 constexpr int kTwoshotMinBlocks = RP_TWOSHOT_MIN_BLOCKS;
+// 16-byte packets per lane per step of the two-shot fold (each loads NR operands)
+#ifndef RP_TWOSHOT_U
+#define RP_TWOSHOT_U(NR) ((NR) > 4 ? 2 : 2)
+#endif
 
 __device__ __forceinline__ bool aligned16(const void* p) { return (((uintptr_t)p) & 15u) == 0; }
 
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, kTwoshotMinBlocks) ar_twoshot_dyn(co
       if (PUSH) in[p] = a.t.data[rank] + a.read_off + ((ptrdiff_t)p - (ptrdiff_t)rank) * (ptrdiff_t)Vc * 16;  // Q_rank[p]
       else in[p] = a.t.data[p] + a.read_off;
     }
-    constexpr int U = NR > 4 ? 1 : 2;
+    constexpr int U = RP_TWOSHOT_U(NR);
     for (uint32_t j = claim_tile(a, rank, 1); j < tpc; j = claim_tile(a, rank, 1)) {
       size_t lo, hi;
       tile_range(rank, j, lo, hi);
