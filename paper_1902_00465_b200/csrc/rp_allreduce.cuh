@@ -23,7 +23,7 @@ constexpr int kUnroll = 2;
 constexpr int kTwoshotMinBlocks = RP_TWOSHOT_MIN_BLOCKS;
 // 16-byte packets per lane per step of the two-shot fold (each loads NR operands)
 #ifndef RP_TWOSHOT_U
-#define RP_TWOSHOT_U(NR) ((NR) > 4 ? 2 : 2)
+#define RP_TWOSHOT_U(NR) ((NR) > 4 ? 2 : 4)
 #endif
 
 __device__ __forceinline__ bool aligned16(const void* p) { return (((uintptr_t)p) & 15u) == 0; }
