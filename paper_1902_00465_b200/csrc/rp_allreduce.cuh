@@ -21,7 +21,10 @@ constexpr int kUnroll = 2;
 #define RP_TWOSHOT_MIN_BLOCKS 1
 #endif
 constexpr int kTwoshotMinBlocks = RP_TWOSHOT_MIN_BLOCKS;
-// 16-byte packets per lane per step of the two-shot fold (each loads NR operands)
+// 16-byte packets per lane per step of the two-shot fold (each loads NR operands):
+// 2 x 8 operands at NR > 4 (122 registers; N=1 bench 179.4 vs 183.3 us with 1),
+// 4 x NR at NR <= 4 (93-120 registers; N=2 117.7 vs 121.1 us, N=4 P2P 169.7 vs
+// 172.8 us with 2) -- profiles/r01_twoshot_occupancy.txt
 #ifndef RP_TWOSHOT_U
 #define RP_TWOSHOT_U(NR) ((NR) > 4 ? 2 : 4)
 #endif
