@@ -25,6 +25,12 @@ here is the same -- each gradient is averaged with the rank-ordered
 Gradient accumulation over several backward passes: wrap all but the last in
 ``opt.no_sync()``; a gradient accumulated again after its bucket was launched is a
 protocol error (the averaged value would be overwritten by a local one).
+
+Measured (profiles/r01_resnet50_overlap.txt): on ResNet-50 over NVLink the
+synchronous exchange costs 0.13-0.19 ms of a 17.3 ms step, while the per-bucket
+cross-stream dependencies this mode needs cost ~0.3 ms and the concurrent exchange
+a little more, so ``overlap=False`` (the default) is faster there. Overlap pays when
+the exchange is a large share of the step.
 """
 
 from __future__ import annotations
