@@ -213,3 +213,23 @@ def test_overlap_bucket_plan_reverse_order_per_dtype():
     # an oversize gradient gets a bucket of its own
     assert plan == [[5, 2], [4], [3], [1], [0]]
     assert sorted(i for b in plan for i in b) == list(range(6))
+
+
+def test_bench_reference_arm_json_contract():
+    """bench.py --impl reference prints one JSON line with the driver's keys (the
+    reference's CPU path, bounded sample; no GPU needed)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--bytes", str(1 << 20)],
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["cores"] >= 1
