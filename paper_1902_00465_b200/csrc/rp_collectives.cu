@@ -690,10 +690,12 @@ int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, si
     void* args[] = {&a, &ivec};
     return rp_launch(c, (const void*)bcast_push_kernel, dim3(blocks), dim3(kThreads), args, 0, stream);
   }
-  // large messages between processes: the pipelined relay (K4r). It lands in the
-  // dst itself when that is pool-resident (symmetric), else in staging
+  // large messages between processes: the pipelined relay (K4r) from 32 MiB, where
+  // its pipeline fill is amortised (below, direct pull / scatter are faster:
+  // profiles/r01_sweep_nccl_final_n4.txt). It lands in the dst itself when that is
+  // pool-resident (symmetric), else in staging
   if (!c->is_virtual && W > 1 && bytes % 16 == 0 &&
-      (algo == RP_ALGO_RELAY || (algo == RP_ALGO_AUTO && bytes > ((size_t)1 << 20) &&
+      (algo == RP_ALGO_RELAY || (algo == RP_ALGO_AUTO && bytes >= ((size_t)32 << 20) &&
                                  getenv("RP_BCAST_PULL") == nullptr))) {
     size_t loff = 0;
     const bool land_dst = symmetric_in_pool(c, (const void* const*)dst, bytes, &loff);
@@ -712,7 +714,11 @@ int rp_launch_broadcast(rp_comm* c, const void* const* src, void* const* dst, si
     a.copy_in = 1;
     a.read_off = scratch;
   }
-  if (algo == RP_ALGO_AUTO) algo = (bytes >= ((size_t)1 << 20) && W > 2) ? RP_ALGO_SCATTER : RP_ALGO_DIRECT;
+  // scatter + all-gather from 8 MiB at N > 2 (2-4 MiB: direct pull is faster, sweep)
+  if (algo == RP_ALGO_AUTO)
+    algo = (bytes >= ((size_t)8 << 20) && W > 2 && !c->is_virtual) || (bytes >= ((size_t)1 << 20) && W > 2 && c->is_virtual)
+               ? RP_ALGO_SCATTER
+               : RP_ALGO_DIRECT;
   if (algo == RP_ALGO_SCATTER) {
     a.write_off = a.copy_in ? scratch + pb : scratch;  // per-rank staging of its chunk
     if (a.write_off + pb > scratch_end) algo = RP_ALGO_DIRECT;
