@@ -76,6 +76,8 @@ def test_c_abi_rejects_bad_arguments_without_a_gpu():
     assert "pool_bytes" in _lib.last_error()
     assert lib.rp_comm_create_virtual(0, 0, 64 << 20, ctypes.byref(ctypes.c_void_p())) == 2
     assert lib.rp_all_reduce(None, None, None, 1, 0, 0, 0, 0, 0, None) == 1            # NULL comm
+    assert lib.rp_comm_set_block_cap(None, 32) == 1                                     # NULL comm
+    assert lib.rp_broadcast(None, None, None, 16, 0, 4, None) == 1                      # relay, NULL comm
 
 
 # --- virtual-replica rendezvous ------------------------------------------------
