@@ -146,7 +146,6 @@ class OverlappedReplicatedOptimizer:
         self.blocks = self.DEFAULT_BLOCKS if blocks is None else int(blocks)
         self._sync = True
         self._draining = False
-        self._launched_any = False
         self._steps = 0
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in uniq]
 
@@ -223,7 +222,6 @@ class OverlappedReplicatedOptimizer:
             self.comm.set_block_cap(0)
         for g in (grads[0] if grads else ()):
             g.record_stream(self.stream)
-        self._launched_any = True
 
     def average_gradients(self):
         """Launch the buckets backward did not complete, then make the compute
