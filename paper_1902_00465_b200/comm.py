@@ -153,6 +153,8 @@ class _Base:
         the copies completed."""
         ins = list(host_in) if isinstance(host_in, (list, tuple)) else [host_in]
         nrep = self.world if isinstance(self, VirtualCommunicator) else 1
+        if nvls and not hasattr(self, "alloc_nvls"):
+            raise errors.ConfigurationError("all_reduce_host(nvls=True) needs a multi-process communicator")
         if len(ins) != nrep:
             raise errors.ShapeError(f"expected {nrep} host tensors, got {len(ins)}")
         x0 = ins[0]
