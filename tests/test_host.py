@@ -235,3 +235,31 @@ def test_bench_reference_arm_json_contract():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_relay_broadcast_tile_partition():
+    """The relay broadcast's index math (csrc/rp_nvls.cu bcast_relay): for every
+    non-root, the tiles it forwards (owner = i mod (N-1) -> rank) and the tiles it
+    receives (j-th tile owned by others) cover every tile exactly once."""
+    for world in range(2, 9):
+        for root in range(world):
+            for nt in (1, 2, world - 1, world, 7 * world + 3):
+                w1 = world - 1
+                for rank in range(world):
+                    if rank == root:
+                        continue
+                    me = rank if rank < root else rank - 1
+                    owned = [me + k * w1 for k in range(nt) if me + k * w1 < nt]
+                    for i in owned:  # the owner mapping of the root agrees
+                        o = i % w1
+                        assert (o if o < root else o + 1) == rank
+                    got = []
+                    if world > 2:
+                        w2 = world - 2
+                        for j in range(nt):
+                            r = j % w2
+                            i = (j // w2) * w1 + (r if r < me else r + 1)
+                            if i >= nt:
+                                break
+                            got.append(i)
+                    assert sorted(owned + got) == list(range(nt)), (world, root, nt, rank)
