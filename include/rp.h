@@ -106,10 +106,47 @@ RP_API int rp_comm_create_virtual(int world, int device, size_t pool_bytes, rp_c
 RP_API size_t rp_comm_export_size(void);
 RP_API int rp_comm_export(rp_comm_t comm, void* buf, size_t* len);
 
-/* `all` = world export blobs concatenated in rank order. Opens every peer's pool
- * over CUDA IPC and checks the topology (peer access between every pair,
- * uniform NVLink); RP_ERR_CONFIG otherwise. */
+/* `all` = world export blobs concatenated in rank order. Discovers the topology
+ * (replaces the reference's MultiGpu device assignment): every
+ * peer's GPU must be visible, CUDA peer access must work, and NVML must report
+ * NVLink P2P to it (NVSwitch gives every pair NVLink) -- rp_topology_check's
+ * policy; RP_ERR_CONFIG (-> ConfigurationError, errors.py:32) otherwise, naming
+ * the pair and the link found. RP_ALLOW_PCIE=1 in the environment accepts PCIe
+ * peer access (tests only). Then opens every peer's pool over CUDA IPC (loopback
+ * peers: the plain pointer). */
 RP_API int rp_comm_import(rp_comm_t comm, const void* all, size_t len);
+
+/* Link kinds rp_comm_import classifies each peer into. */
+enum {
+  RP_LINK_SELF = 0,
+  RP_LINK_NVLINK = 1,      /* CUDA peer access + NVML NVLink P2P                  */
+  RP_LINK_PCIE = 2,        /* peer access, but NVML reports no NVLink              */
+  RP_LINK_NONE = 3,        /* no CUDA peer access                                 */
+  RP_LINK_UNKNOWN = 4,     /* peer not visible, or NVML unavailable               */
+  RP_LINK_SAME_DEVICE = 5, /* another process on this GPU                          */
+  RP_LINK_LOOPBACK = 6,    /* a rank of this process's loopback world (same GPU)  */
+};
+
+/* The topology policy rp_comm_import applies to this rank's row of links
+ * (links[p] = RP_LINK_* to rank p): NVLINK everywhere; PCIE only with
+ * allow_pcie; LOOPBACK only in a loopback world. RP_ERR_CONFIG with the offending
+ * pair in rp_last_error() otherwise. Pure host logic (no device needed). */
+RP_API int rp_topology_check(int world, int rank, const int* links, int allow_pcie, int loopback);
+
+/* Loopback world (testing the multi-process kernels on ONE GPU): `world`
+ * non-virtual communicators created in ONE process on the same device, each
+ * driven from its own host thread and stream, exchange blobs in-process and set
+ * this BEFORE rp_comm_import. Peers' regions are then plain pointers (no IPC) and
+ * every rank's grids are capped at num_sms / world blocks so all ranks' blocks
+ * are co-resident. Same kernels, same barriers, same pool layout as one process
+ * per GPU; the NVLink hop is replaced by local HBM. */
+RP_API int rp_comm_set_loopback(rp_comm_t comm, int on);
+
+/* Make `device`'s stream-ordered memory pools safe for a loopback world (call once,
+ * before the ranks allocate): no cross-stream reuse through inserted waits
+ * (cudaMemPoolReuseAllowInternalDependencies = 0), which could make one rank's
+ * stream wait behind a peer's collective kernel that waits for this rank. */
+RP_API int rp_loopback_prepare(int device);
 
 RP_API int rp_comm_destroy(rp_comm_t comm);
 
@@ -125,8 +162,11 @@ RP_API int rp_comm_info(rp_comm_t comm, int* rank, int* world, int* is_virtual, 
  * staging uses the rest. Must be called identically on every rank. */
 RP_API int rp_comm_reserve(rp_comm_t comm, size_t bytes);
 
-/* Synchronise the device and report a collective abort/timeout recorded by the
- * kernels (RP_ERR_ABORTED with the reason), then clear it. */
+/* Synchronise the device (a loopback rank does not: its caller synchronises the
+ * streams it launched on, since a device-wide sync could wait on a peer kernel
+ * that waits for this rank's next launch) and report a collective abort/timeout
+ * recorded by the kernels (RP_ERR_ABORTED with the reason). The abort is sticky:
+ * a communicator that aborted stays aborted. */
 RP_API int rp_comm_check(rp_comm_t comm);
 
 /* Spin timeout for cross-rank waits, nanoseconds (default 20 s). */
@@ -243,11 +283,13 @@ RP_API int rp_bn_apply(const void* x, void* y, int dtype, int64_t rows, int64_t 
                 const float* mean, const float* invstd, const float* weight, const float* bias,
                 void* stream);
 
-/* Elementwise BN backward: dx = (dy - sum_dy/M - (x-mean)*invstd^2*sum_dy_xmu/M)*invstd*w. */
+/* Elementwise BN backward: dx = (dy - sum_dy/M - (x-mean)*invstd^2*sum_dy_xmu/M)*invstd*w.
+ * M = *count_device (the device f64 scalar rp_bn_stats wrote; no host sync) when
+ * count_device is non-NULL, else count_total. */
 RP_API int rp_bn_bwd_apply(const void* x, const void* dy, void* dx, int dtype, int64_t rows, int64_t c,
                     int64_t hw, int layout, const float* mean, const float* invstd,
                     const float* weight, const float* sum_dy, const float* sum_dy_xmu,
-                    double count_total, void* stream);
+                    double count_total, const double* count_device, void* stream);
 
 /* ---- fusion-buffer packing (K6) ------------------------------------------ */
 

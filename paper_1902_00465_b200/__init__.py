@@ -9,11 +9,14 @@ duck type and Replicator API. See DESIGN.md.
 
 from . import errors
 from ._lib import load as load_library
+from .bootstrap import DistBootstrap, LoopbackWorld
 from .comm import Communicator, VirtualCommunicator
 from .replicator import CrossReplicaBatchNorm, PerReplica, ReplicatedOptimizer, Replicator
 
 __all__ = [
     "Communicator",
+    "DistBootstrap",
+    "LoopbackWorld",
     "VirtualCommunicator",
     "Replicator",
     "ReplicatedOptimizer",

@@ -29,6 +29,8 @@ RELAY = 4
 OPT_SGD, OPT_ADAM, OPT_ADAMW = 0, 1, 2
 ALGOS = {"auto": AUTO, "oneshot": ONESHOT, "twoshot": TWOSHOT, "direct": DIRECT, "scatter": SCATTER, "nvls": NVLS,
          "relay": RELAY}
+# link kinds (rp_comm_import topology discovery, rp_topology_check)
+LINK_SELF, LINK_NVLINK, LINK_PCIE, LINK_NONE, LINK_UNKNOWN, LINK_SAME_DEVICE, LINK_LOOPBACK = range(7)
 # layouts
 NHWC, NCHW = 0, 1
 # status codes -> exception classes (errors.py)
@@ -58,6 +60,9 @@ SIGNATURES = {
     "rp_comm_export_size": (_size_t, []),
     "rp_comm_export": (_i, [_c_void_p, _c_void_p, ctypes.POINTER(_size_t)]),
     "rp_comm_import": (_i, [_c_void_p, _c_void_p, _size_t]),
+    "rp_comm_set_loopback": (_i, [_c_void_p, _i]),
+    "rp_loopback_prepare": (_i, [_i]),
+    "rp_topology_check": (_i, [_i, _i, ctypes.POINTER(_i), _i, _i]),
     "rp_comm_destroy": (_i, [_c_void_p]),
     "rp_comm_pool": (_i, [_c_void_p, _i, _pp, ctypes.POINTER(_size_t)]),
     "rp_comm_info": (_i, [_c_void_p, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i),
@@ -86,7 +91,7 @@ SIGNATURES = {
     "rp_bn_apply": (_i, [_c_void_p, _c_void_p, _i, _i64, _i64, _i64, _i, _c_void_p, _c_void_p,
                          _c_void_p, _c_void_p, _c_void_p]),
     "rp_bn_bwd_apply": (_i, [_c_void_p, _c_void_p, _c_void_p, _i, _i64, _i64, _i64, _i, _c_void_p,
-                             _c_void_p, _c_void_p, _c_void_p, _c_void_p, _d, _c_void_p]),
+                             _c_void_p, _c_void_p, _c_void_p, _c_void_p, _d, _c_void_p, _c_void_p]),
     "rp_nvls_create": (_i, [_c_void_p, _size_t, ctypes.c_char_p, _size_t]),
     "rp_nvls_serve": (_i, [_c_void_p]),
     "rp_nvls_join": (_i, [_c_void_p, ctypes.c_char_p]),

@@ -17,8 +17,9 @@ values are copied in and out around the kernel.
 MultiDevice replication, whose stitched folds are graph.py:506-540 -- and runs each
 collective as one cooperative kernel over all replicas' buffers.
 
-Bootstrap uses ``torch.distributed`` only to exchange the CUDA IPC handle blobs;
-no NCCL call sits on any collective path.
+Bootstrap (bootstrap.py) exchanges only the CUDA IPC handle blobs -- over
+``torch.distributed`` between processes, or in-process for a loopback world; no
+NCCL call sits on any collective path.
 """
 
 from __future__ import annotations
@@ -55,9 +56,6 @@ def dtype_code(dt) -> int:
     return code
 
 
-def _stream_handle(device) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
-
 
 class _DevBuf:
     """``__cuda_array_interface__`` view of device memory owned by a communicator."""
@@ -75,15 +73,28 @@ def tensor_at(ptr: int, numel: int, dtype: torch.dtype, device: int, owner) -> t
     return raw.view(dtype)
 
 
-def exchange_blobs(blob: bytes, group=None) -> bytes:
-    """Bootstrap exchange: every rank's export blob, concatenated in rank order.
-    The only use of torch.distributed (any backend); never on a data path."""
-    import torch.distributed as dist
+def to_host(t: torch.Tensor) -> torch.Tensor:
+    """Device -> host through pinned memory on the current stream, then synchronise
+    that stream only. A pageable device->host copy may wait on OTHER streams'
+    kernels: in a loopback world that includes a peer kernel waiting for this
+    rank's next launch (measured: W=8 stalled until the spin timeout; pinned
+    copies never did). Pinned is also the fast path."""
+    if not t.is_cuda:
+        return t
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h
 
-    world = dist.get_world_size(group)
-    blobs = [None] * world
-    dist.all_gather_object(blobs, bytes(blob), group=group)
-    if any(len(b) != len(blob) for b in blobs):
+
+def exchange_blobs(blob: bytes, bootstrap=None) -> bytes:
+    """Bootstrap exchange: every rank's export blob, concatenated in rank order,
+    over ``bootstrap`` (default: the torch.distributed group). Never on a data path."""
+    if bootstrap is None:
+        from .bootstrap import DistBootstrap
+        bootstrap = DistBootstrap()
+    blobs = bootstrap.all_gather_object(bytes(blob))
+    if any(not isinstance(b, bytes) or len(b) != len(blob) for b in blobs):
         raise errors.ProtocolError("ranks exported blobs of different sizes (mismatched library builds?)")
     return b"".join(blobs)
 
@@ -117,9 +128,35 @@ class _Base:
         except Exception:
             pass
 
+    # -- launch ordering -------------------------------------------------------
+    _last_stream = None
+
+    def _stream(self) -> int:
+        """Stream handle for the next collective launch, ordered after this
+        communicator's previous collective. Every kernel of a communicator shares
+        its device-side sequencing state (tile counters, phase rows, epochs), so two
+        of them must never run concurrently on one rank -- e.g. an overlapped bucket
+        all-reduce on the side stream (overlap.py) and a BN exchange on the compute
+        stream. When a launch comes from a different stream than the previous one,
+        the new stream first waits for the old one; launches from one stream are
+        ordered already. Ranks issue collectives in the same program order, so the
+        device order pairs the same calls on every rank."""
+        cur = torch.cuda.current_stream(self.device)
+        last = self._last_stream
+        if last is not None and last != cur:
+            cur.wait_stream(last)
+        self._last_stream = cur
+        return cur.cuda_stream
+
     def check(self):
         """Synchronise and raise ``CollectiveAbortedError`` if a kernel timed out or a
-        peer aborted (include/rp.h rp_comm_check)."""
+        peer aborted (include/rp.h rp_comm_check). Waits for this communicator's
+        own launches (the streams it launched on), never for a device-wide sync
+        that could wait on a loopback peer's kernel."""
+        dev = torch.device(f"cuda:{self.device}")
+        torch.cuda.current_stream(dev).synchronize()
+        if self._last_stream is not None:
+            self._last_stream.synchronize()
         _lib.check(self._lib.rp_comm_check(self._handle), "collective")
 
     def set_timeout(self, seconds: float):
@@ -251,26 +288,35 @@ class Communicator(_Base):
     """
 
     def __init__(self, group=None, device: int | None = None, pool_bytes: int = DEFAULT_POOL_BYTES,
-                 timeout_s: float = 20.0):
+                 timeout_s: float = 20.0, bootstrap=None):
+        """``bootstrap``: how the ranks find each other (bootstrap.py). Default: the
+        initialised torch.distributed group ``group`` (one process per GPU), or a
+        single rank when torch.distributed is not initialised. A loopback world's
+        ``world.bootstrap(rank)`` puts every rank in this process on one device."""
         import torch.distributed as dist
 
+        from .bootstrap import DistBootstrap
+
         lib = _lib.load()
-        if dist.is_available() and dist.is_initialized():
-            rank, world = dist.get_rank(group), dist.get_world_size(group)
-        else:
-            rank, world = 0, 1
+        if bootstrap is None and dist.is_available() and dist.is_initialized():
+            bootstrap = DistBootstrap(group)
+        rank, world = (bootstrap.rank, bootstrap.world) if bootstrap is not None else (0, 1)
         if device is None:
             device = torch.cuda.current_device()
         self.rank, self.world, self.device = rank, world, int(device)
+        self.bootstrap = bootstrap
+        self.loopback = bool(getattr(bootstrap, "loopback", False))
         h = ctypes.c_void_p()
         _lib.check(lib.rp_comm_create(rank, world, self.device, pool_bytes, ctypes.byref(h)), "comm_create")
         self._handle = h
         if world > 1:
+            if self.loopback:
+                _lib.check(lib.rp_comm_set_loopback(h, 1), "comm_set_loopback")
             size = lib.rp_comm_export_size()
             buf = ctypes.create_string_buffer(size)
             n = ctypes.c_size_t(size)
             _lib.check(lib.rp_comm_export(h, buf, ctypes.byref(n)), "comm_export")
-            joined = exchange_blobs(bytes(buf.raw[: n.value]), group)
+            joined = exchange_blobs(bytes(buf.raw[: n.value]), bootstrap)
             _lib.check(lib.rp_comm_import(h, joined, len(joined)), "comm_import")
         self._init_common(pool_bytes, timeout_s)
 
@@ -288,26 +334,24 @@ class Communicator(_Base):
     # -- NVLS (NVLink SHARP) region -------------------------------------------
     def enable_nvls(self, nbytes: int, group=None) -> None:
         """Bind ``nbytes`` of this rank's memory to one multicast object spanning all
-        ranks (include/rp.h rp_nvls_*). Collective over the group; the multicast fd
-        travels from rank 0 over a Unix socket, its name over torch.distributed."""
-        import torch.distributed as dist
-
+        ranks (include/rp.h rp_nvls_*). Collective over the bootstrap; the multicast
+        fd travels from rank 0 over a Unix socket, its name over the bootstrap."""
         if self.world < 2:
             raise errors.ConfigurationError("NVLS needs at least two ranks")
+        if self.loopback:
+            raise errors.ConfigurationError("NVLS needs one process per GPU (a multicast object spans distinct "
+                                            "devices; a loopback world has one)")
         name = ctypes.create_string_buffer(128)
         _lib.check(self._lib.rp_nvls_create(self._handle, nbytes, name, 128), "nvls_create")
-        names = [None]
-        if self.rank == 0:
-            names = [name.value]
-        dist.broadcast_object_list(names, src=0, group=group)
+        root_name = self.bootstrap.broadcast_object(name.value if self.rank == 0 else None, src=0)
         if self.rank == 0:
             _lib.check(self._lib.rp_nvls_serve(self._handle), "nvls_serve")
         else:
-            _lib.check(self._lib.rp_nvls_join(self._handle, names[0]), "nvls_join")
+            _lib.check(self._lib.rp_nvls_join(self._handle, root_name), "nvls_join")
         _lib.check(self._lib.rp_nvls_add(self._handle), "nvls_add")
-        dist.barrier(group=group)
+        self.bootstrap.barrier()
         _lib.check(self._lib.rp_nvls_bind(self._handle), "nvls_bind")
-        dist.barrier(group=group)
+        self.bootstrap.barrier()
         base = ctypes.c_void_p()
         size = ctypes.c_size_t()
         _lib.check(self._lib.rp_nvls_pool(self._handle, ctypes.byref(base), ctypes.byref(size)), "nvls_pool")
@@ -334,9 +378,6 @@ class Communicator(_Base):
         return tensor_at(self._nvls_base + off, numel, dtype, self.device, self)
 
     # -- torch-tensor collectives ------------------------------------------
-    def _stream(self):
-        return _stream_handle(self.device)
-
     def all_reduce_tensor(self, x: torch.Tensor, kind: str = "sum", out: torch.Tensor | None = None,
                           comm_dtype: torch.dtype | None = None, algo: str = "auto") -> torch.Tensor:
         """out = kind-fold of x over ranks (ascending rank order, graph.py:514-533).
@@ -381,7 +422,7 @@ class Communicator(_Base):
             x = x.reshape(1)
         tail = hashlib.sha256(repr((tuple(x.shape[1:]), str(x.dtype))).encode()).digest()[:8]
         meta = torch.tensor([x.shape[0], int.from_bytes(tail, "little", signed=True)], dtype=torch.int64)
-        g = self.all_gather_tensor(meta.to(x.device)).cpu()
+        g = to_host(self.all_gather_tensor(meta.to(x.device)))
         for r in range(self.world):
             if int(g[r, 1]) != int(g[self.rank, 1]):
                 raise errors.ProtocolError(f"all_gather: rank {r} and rank {self.rank} differ beyond the leading "
@@ -431,7 +472,7 @@ class Communicator(_Base):
             self._tensor_cls = type(local)
         x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
         y = self.all_reduce_tensor(x, kind)
-        return wrap(y.cpu().numpy())
+        return wrap(to_host(y).numpy())
 
     def all_gather(self, local, label=None):
         """[t_0, ..., t_{N-1}] in rank order; leading dimensions may differ across
@@ -445,9 +486,9 @@ class Communicator(_Base):
         arr, wrap = _host_in(local)
         x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
         if x.dim() == 0:
-            g = self.all_gather_tensor(x.reshape(1)).cpu().numpy()
+            g = to_host(self.all_gather_tensor(x.reshape(1))).numpy()
             return [wrap(g[r, 0]) for r in range(self.world)]
-        return [wrap(t.cpu().numpy()) for t in self.all_gather_ragged(x)]
+        return [wrap(to_host(t).numpy()) for t in self.all_gather_ragged(x)]
 
     def broadcast(self, root_value, label=None, shape=None, dtype=None, root: int = 0):
         """Reference form (graph.py:580-582): root passes its value, others pass None
@@ -470,7 +511,7 @@ class Communicator(_Base):
                 self._tensor_cls = type(root_value)
         x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}")
         y = self.broadcast_tensor(x, root)
-        return wrap(y.cpu().numpy())
+        return wrap(to_host(y).numpy())
 
     # -- protocol agreement (debug): every rank must issue the same collective
     def verify(self, label: str, kind: str, shape, dtype, position=None) -> None:
@@ -482,7 +523,7 @@ class Communicator(_Base):
         desc = repr((position, label, kind, tuple(shape), str(dtype)))
         h = hashlib.sha256(desc.encode()).digest()[:16]
         t = torch.frombuffer(bytearray(h), dtype=torch.uint8).to(f"cuda:{self.device}")
-        g = self.all_gather_tensor(t).cpu()
+        g = to_host(self.all_gather_tensor(t))
         bad = [r for r in range(self.world) if not torch.equal(g[r], g[self.rank])]
         if bad:
             # second exchange (every rank takes this branch: some rank disagrees with
@@ -490,7 +531,7 @@ class Communicator(_Base):
             raw = desc.encode()[:240]
             buf = torch.zeros(256, dtype=torch.uint8)
             buf[: len(raw)] = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
-            d = self.all_gather_tensor(buf.to(f"cuda:{self.device}")).cpu()
+            d = to_host(self.all_gather_tensor(buf.to(f"cuda:{self.device}")))
             other = bytes(d[bad[0]].numpy()).rstrip(b"\0").decode(errors="replace")
             raise errors.ProtocolError(f"collective protocol mismatch: rank {self.rank} issued {desc}, "
                                        f"rank {bad[0]} issued {other} (ranks {bad} disagree with rank {self.rank})")
@@ -548,7 +589,7 @@ class VirtualCommunicator(_Base):
         dp, _k2 = _lib.ptr_array([o.data_ptr() for o in outs])
         _lib.check(self._lib.rp_all_reduce_v(self._handle, sp, dp, xs[0].numel(), code, ccode,
                                              dtype_code(outs[0].dtype), _op(kind), _algo(algo),
-                                             _stream_handle(self.device)), "all_reduce")
+                                             self._stream()), "all_reduce")
         return outs
 
     def all_gather(self, xs, outs=None, label=None):
@@ -561,7 +602,7 @@ class VirtualCommunicator(_Base):
         sp, _k1 = _lib.ptr_array([x.data_ptr() for x in xs])
         dp, _k2 = _lib.ptr_array([o.data_ptr() for o in outs])
         _lib.check(self._lib.rp_all_gather_v(self._handle, sp, dp, xs[0].numel() * xs[0].element_size(),
-                                             _stream_handle(self.device)), "all_gather")
+                                             self._stream()), "all_gather")
         return outs
 
     def all_gather_ragged(self, xs):
@@ -600,7 +641,7 @@ class VirtualCommunicator(_Base):
         sp, _k1 = _lib.ptr_array([x.data_ptr() for x in xs])
         dp, _k2 = _lib.ptr_array([o.data_ptr() for o in outs])
         _lib.check(self._lib.rp_broadcast_v(self._handle, sp, dp, xs[0].numel() * xs[0].element_size(), root,
-                                            _algo(algo), _stream_handle(self.device)), "broadcast")
+                                            _algo(algo), self._stream()), "broadcast")
         return outs
 
 

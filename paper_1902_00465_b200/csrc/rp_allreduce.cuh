@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(kThreads, kTwoshotMinBlocks) ar_twoshot_dyn(co
   using T = typename DType<DT>::T;
   using A = typename DType<DT>::Acc;
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
   const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
   const size_t Vc = a.chunk;
   const uint32_t tv = a.tile_v;
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(kThreads) ar_oneshot_push(const CollArgs a) {
   using T = typename DType<DT>::T;
   using A = typename DType<DT>::Acc;
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
   const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
   const size_t sub = (V + gridDim.x - 1) / gridDim.x;
   const size_t lo = (size_t)blockIdx.x * sub;
@@ -400,6 +402,7 @@ __global__ void __launch_bounds__(kThreads) ar_oneshot(const CollArgs a) {
   using A = typename DType<DT>::Acc;
   constexpr int kUnroll = NR > 4 ? 1 : 2;  // latency regime: keep registers for NR loads
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
   const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
   const size_t sub = (V + gridDim.x - 1) / gridDim.x;
   const size_t lo = (size_t)blockIdx.x * sub;

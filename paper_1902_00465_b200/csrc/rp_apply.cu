@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kThreads) ar_apply(const ApplyArgs x) {
   constexpr int E = 16 / sizeof(T);  // elements per gradient packet (f32 params: E floats)
   const CollArgs& a = x.a;
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
   const int local = a.rank >= 0 ? 0 : rank;  // index into the per-local-replica pointer arrays
   const size_t V = (a.count + E - 1) / E;
   const size_t Vc = a.chunk;

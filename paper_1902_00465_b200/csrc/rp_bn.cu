@@ -424,7 +424,9 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
 }
 
 __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
-  exchange_body(a, a.rank >= 0 ? a.rank : (int)blockIdx.y, blockIdx.x, gridDim.x);
+  const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
+  exchange_body(a, rank, blockIdx.x, gridDim.x);
 }
 
 // --- fused statistics (NHWC): the local pass and the cross-replica reduction in
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_stats_fused(const FusedBnArgs f
     } while ((int32_t)(v - (base + total)) < 0);
   }
   __syncthreads();
-  if ((int)bid >= f.ex_blocks) return;
+  if ((int)bid >= f.ex_blocks || rp_aborted(f.e.t, rank)) return;
   exchange_body(f.e, rank, (int)bid, f.ex_blocks);
   if (bid == 0 && threadIdx.x == 0) state_store(f.e.t, rank, RP_ST_BN_GRID_BASE, base + total);
 }
@@ -476,8 +478,10 @@ __global__ void __launch_bounds__(kBnThreads) bn_apply_kernel(const T* __restric
                                                               const float* __restrict__ invstd,
                                                               const float* __restrict__ w, const float* __restrict__ b,
                                                               const float* __restrict__ sum_dy,
-                                                              const float* __restrict__ sum_dy_xmu, float inv_m) {
+                                                              const float* __restrict__ sum_dy_xmu,
+                                                              const double* __restrict__ count, float inv_m) {
   constexpr int VEC = 16 / sizeof(T);
+  if (BWD && count) inv_m = (float)(1.0 / *count);  // M on the device: no host sync
   const bool vec = (((((uintptr_t)x) | ((uintptr_t)y) | (BWD ? (uintptr_t)dy : 0)) & 15u) == 0) &&
                    (nchw ? (hw % VEC == 0) : (C % VEC == 0));
   auto coef = [&](int64_t ch, float& m, float& s, float& k1, float& k2) {
@@ -565,8 +569,9 @@ __global__ void __launch_bounds__(kBnThreads) bn_apply_nhwc_rc(
     const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ y, int64_t total, int64_t C,
     const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ w,
     const float* __restrict__ b, const float* __restrict__ sum_dy, const float* __restrict__ sum_dy_xmu,
-    float inv_m) {
+    const double* __restrict__ count, float inv_m) {
   constexpr int VEC = 16 / sizeof(T);
+  if (BWD && count) inv_m = (float)(1.0 / *count);
   constexpr int U = 4;
   const int64_t nv = total / VEC;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -622,16 +627,26 @@ using namespace rp;
 
 namespace {
 
-int ensure_partials(rp_comm* c, size_t bytes) {
+// Per-split f64 partials. Grown geometrically and never freed before the
+// communicator (an earlier launch on another stream may still read the old
+// buffer), so no device-wide synchronisation: it would deadlock a loopback world,
+// whose peers wait on this rank's next kernel. Growing inside a CUDA-graph capture
+// is refused (run the step once eagerly first, as graph capture requires anyway).
+int ensure_partials(rp_comm* c, size_t bytes, cudaStream_t stream) {
   if (bytes <= c->bn_partials_bytes) return RP_OK;
-  if (c->bn_partials) {
-    cudaDeviceSynchronize();
-    cudaFree(c->bn_partials);
-    c->bn_partials = nullptr;
-    c->bn_partials_bytes = 0;
-  }
-  RP_CUDA_CHECK(cudaMalloc(&c->bn_partials, bytes));
-  c->bn_partials_bytes = bytes;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone)
+    return rp_fail(RP_ERR_INVALID, "bn: statistics scratch must grow (" + std::to_string(bytes) +
+                                       " bytes) during CUDA-graph capture; run the step once before capturing");
+  size_t want = std::max<size_t>(bytes, std::max<size_t>(2 * c->bn_partials_bytes, (size_t)4 << 20));
+  double* p = nullptr;
+  // stream-ordered: no implicit device-wide wait (cudaMalloc may wait for the
+  // whole device, i.e. for a loopback peer's kernel waiting on this rank)
+  RP_CUDA_CHECK(cudaMallocAsync((void**)&p, want, stream));
+  if (c->bn_partials) c->bn_retired.push_back(c->bn_partials);
+  c->bn_partials = p;
+  c->bn_partials_bytes = want;
   return RP_OK;
 }
 
@@ -713,7 +728,7 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBnThreads, smem0) != cudaSuccess || per_sm < 1)
       per_sm = 2;
   }
-  const int target = per_sm * c->num_sms / nrep;
+  const int target = (int)rp_wave_per_rank(c, per_sm);
   if (layout == RP_LAYOUT_NHWC) {
     block = dim3(kBnThreads);
     const int64_t cvt = ch / nv;  // channel-vectors per row
@@ -743,7 +758,7 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
       RP_CUDA_CHECK(cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int fper = 0;
     RP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fper, ff, kBnThreads, smem));
-    const int64_t wave = (int64_t)fper * c->num_sms / nrep;  // co-resident blocks per replica
+    const int64_t wave = rp_wave_per_rank(c, fper);  // co-resident blocks per replica
     if ((int64_t)grid.x * grid.y > wave) grid.y = (unsigned)std::max<int64_t>(1, wave / grid.x);
     const int64_t emax = std::min<int64_t>(RP_BN_ROWS, wave);
     while (fcpb < kExThreads && (ch + fcpb - 1) / fcpb > emax) fcpb *= 2;
@@ -753,7 +768,7 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
     if (fused) a.S = (int)grid.y;
   }
   const size_t per_rep = (size_t)a.S * ch * 2 * sizeof(double);
-  int rc = ensure_partials(c, per_rep * nrep);
+  int rc = ensure_partials(c, per_rep * nrep, stream);
   if (rc) return rc;
   for (int i = 0; i < nrep; ++i) a.part[i] = c->bn_partials + (per_rep / sizeof(double)) * i;
   if (smem > 48 * 1024) {
@@ -801,7 +816,11 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
     fa.e = e;
     fa.ex_blocks = fex;
     void* fargs[] = {&fa};
-    RP_CUDA_CHECK(cudaLaunchCooperativeKernel(ff, grid, block, fargs, smem, stream));
+    // the grid is one co-resident wave (checked above); a loopback world shares the
+    // device with its peers' kernels, so it relies on the block cap instead of the
+    // cooperative launch's whole-device guarantee
+    if (c->loopback) RP_CUDA_CHECK(cudaLaunchKernel(ff, grid, block, fargs, smem, stream));
+    else RP_CUDA_CHECK(cudaLaunchCooperativeKernel(ff, grid, block, fargs, smem, stream));
     return RP_OK;
   }
   // exchange geometry: as many blocks as the BN signal rows and co-residency allow,
@@ -850,7 +869,7 @@ int64_t gcd64(int64_t a, int64_t b) {
 template <bool BWD>
 bool launch_apply_rc(int dtype, const void* x, const void* dy, void* y, int64_t total, int64_t C, const float* mean,
                      const float* invstd, const float* w, const float* b, const float* sdy, const float* sdx,
-                     float inv_m, int sms, cudaStream_t stream) {
+                     const double* cnt, float inv_m, int sms, cudaStream_t stream) {
   const int vec = (int)(16 / rp_dtype_size(dtype));
   if (C % vec || total % vec) return false;
   if ((((uintptr_t)x) | ((uintptr_t)y) | (BWD ? (uintptr_t)dy : 0)) & 15u) return false;
@@ -867,7 +886,7 @@ bool launch_apply_rc(int dtype, const void* x, const void* dy, void* y, int64_t 
     default: return false;
   }
   void* args[] = {(void*)&x, (void*)&dy, (void*)&y, (void*)&total, (void*)&C, (void*)&mean, (void*)&invstd,
-                  (void*)&w, (void*)&b, (void*)&sdy, (void*)&sdx, (void*)&inv_m};
+                  (void*)&w, (void*)&b, (void*)&sdy, (void*)&sdx, (void*)&cnt, (void*)&inv_m};
   return cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(kBnThreads), args, 0, stream) == cudaSuccess;
 }
 
@@ -889,18 +908,19 @@ int rp_bn_apply(const void* x, void* y, int dtype, int64_t rows, int64_t ch, int
     default: return rp_fail(RP_ERR_INVALID, "bn_apply: dtype must be f32/bf16/f16");
   }
   const void* dy = nullptr;
+  const double* no_count = nullptr;
   float inv_m = 0.0f;
   int64_t C = ch, HW = hw;
   void* args[] = {(void*)&x, (void*)&dy, (void*)&y, (void*)&total, (void*)&C, (void*)&HW, (void*)&nchw,
                   (void*)&mean, (void*)&invstd, (void*)&weight, (void*)&bias, (void*)&none, (void*)&none,
-                  (void*)&inv_m};
+                  (void*)&no_count, (void*)&inv_m};
   int rc = rp_set_device_from_ptr(x);
   if (rc) return rc;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (!nchw && launch_apply_rc<false>(dtype, x, nullptr, y, total, ch, mean, invstd, weight, bias, nullptr, nullptr,
-                                      0.0f, sms, (cudaStream_t)stream))
+                                      nullptr, 0.0f, sms, (cudaStream_t)stream))
     return RP_OK;
   const int blocks = (int)std::min<int64_t>((total / 8 + kBnThreads - 1) / kBnThreads + 1, (int64_t)sms * 8);
   RP_CUDA_CHECK(cudaLaunchKernel(fn, dim3(blocks), dim3(kBnThreads), args, 0, (cudaStream_t)stream));
@@ -909,7 +929,7 @@ int rp_bn_apply(const void* x, void* y, int dtype, int64_t rows, int64_t ch, int
 
 int rp_bn_bwd_apply(const void* x, const void* dy, void* dx, int dtype, int64_t rows, int64_t ch, int64_t hw,
                     int layout, const float* mean, const float* invstd, const float* weight, const float* sum_dy,
-                    const float* sum_dy_xmu, double count_total, void* stream) {
+                    const float* sum_dy_xmu, double count_total, const double* count_device, void* stream) {
   const int64_t total = rows * ch * hw;
   if (total == 0) return RP_OK;
   const int nchw = layout == RP_LAYOUT_NCHW;
@@ -921,18 +941,19 @@ int rp_bn_bwd_apply(const void* x, const void* dy, void* dx, int dtype, int64_t 
     case RP_F16: fn = (const void*)bn_apply_kernel<__half, true>; break;
     default: return rp_fail(RP_ERR_INVALID, "bn_bwd_apply: dtype must be f32/bf16/f16");
   }
-  float inv_m = (float)(1.0 / count_total);
+  if (!count_device && !(count_total > 0)) return rp_fail(RP_ERR_INVALID, "bn_bwd_apply: count must be > 0");
+  float inv_m = count_device ? 0.0f : (float)(1.0 / count_total);
   int64_t C = ch, HW = hw;
   void* args[] = {(void*)&x, (void*)&dy, (void*)&dx, (void*)&total, (void*)&C, (void*)&HW, (void*)&nchw,
                   (void*)&mean, (void*)&invstd, (void*)&weight, (void*)&none, (void*)&sum_dy, (void*)&sum_dy_xmu,
-                  (void*)&inv_m};
+                  (void*)&count_device, (void*)&inv_m};
   int rc = rp_set_device_from_ptr(x);
   if (rc) return rc;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (!nchw && launch_apply_rc<true>(dtype, x, dy, dx, total, ch, mean, invstd, weight, nullptr, sum_dy, sum_dy_xmu,
-                                     inv_m, sms, (cudaStream_t)stream))
+                                     count_device, inv_m, sms, (cudaStream_t)stream))
     return RP_OK;
   const int blocks = (int)std::min<int64_t>((total / 8 + kBnThreads - 1) / kBnThreads + 1, (int64_t)sms * 8);
   RP_CUDA_CHECK(cudaLaunchKernel(fn, dim3(blocks), dim3(kBnThreads), args, 0, (cudaStream_t)stream));

@@ -77,6 +77,7 @@ __device__ __forceinline__ void copy_bytes(char* dst, const char* src, size_t lo
 // a.count = bytes per rank, a.chunk = per-block byte slice (multiple of 16).
 __global__ void __launch_bounds__(kThreads) allgather_kernel(const CollArgs a, size_t read_stride, int vec) {
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
   const size_t B = a.count;
   const size_t lo = (size_t)blockIdx.x * a.chunk;
   const size_t hi = std::min(lo + a.chunk, B);
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(kThreads) allgather_kernel(const CollArgs a, s
 // multiple, slots * world <= RP_OS_REGION), a.write_off = per-block byte slice.
 __global__ void __launch_bounds__(kThreads) allgather_push_kernel(const CollArgs a, int vec) {
   const int rank = a.rank;
+  if (rp_aborted(a.t, rank)) return;
   const size_t B = a.count;
   const size_t lo = (size_t)blockIdx.x * a.write_off;
   const size_t hi = std::min(lo + a.write_off, B);
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(kThreads) allgather_push_kernel(const CollArgs
 // zones and parity protocol as K1p / K3p. a.write_off = per-block byte slice.
 __global__ void __launch_bounds__(kThreads) bcast_push_kernel(const CollArgs a, int vec) {
   const int rank = a.rank;
+  if (rp_aborted(a.t, rank)) return;
   const size_t B = a.count;
   const size_t lo = (size_t)blockIdx.x * a.write_off;
   const size_t hi = std::min(lo + a.write_off, B);
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(kThreads) bcast_push_kernel(const CollArgs a, 
 // K4a: direct broadcast: every rank pulls root's pool copy.
 __global__ void __launch_bounds__(kThreads) bcast_direct_kernel(const CollArgs a, int vec) {
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
   const size_t B = a.count;
   const size_t lo = (size_t)blockIdx.x * a.chunk;
   const size_t hi = std::min(lo + a.chunk, B);
@@ -180,6 +184,7 @@ __global__ void __launch_bounds__(kThreads) bcast_direct_kernel(const CollArgs a
 // bytes (multiple of 16*gridDim.x); block b owns slice b of every chunk.
 __global__ void __launch_bounds__(kThreads) bcast_scatter_kernel(const CollArgs a, size_t C, int vec) {
   const int rank = a.rank >= 0 ? a.rank : (int)blockIdx.y;
+  if (rp_aborted(a.t, rank)) return;
   const size_t B = a.count;
   const size_t s0 = (size_t)blockIdx.x * a.chunk;
   const size_t s1 = std::min(s0 + a.chunk, C);

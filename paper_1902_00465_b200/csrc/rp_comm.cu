@@ -8,9 +8,14 @@
 // resolve over NVLink/NVSwitch. Replaces the reference's transport layer
 // and its communicator (graph.py:565-583).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvml.h>
+#include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -54,8 +59,15 @@ int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want) {
   int cap = occ * c->num_sms;
   if (c->is_virtual) cap /= c->world;
   cap = std::min(cap, RP_MAX_BLOCKS);
-  if (c->block_cap > 0) cap = std::min(cap, c->block_cap);
+  if (c->cap() > 0) cap = std::min(cap, c->cap());
   return std::max(1, std::min(want, cap));
+}
+
+int64_t rp_wave_per_rank(rp_comm* c, int per_sm) {
+  int64_t w = (int64_t)std::max(per_sm, 1) * c->num_sms;
+  if (c->is_virtual) w /= c->world;
+  if (c->cap() > 0) w = std::min<int64_t>(w, c->cap());
+  return std::max<int64_t>(w, 1);
 }
 
 int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, size_t smem,
@@ -191,10 +203,114 @@ static int pack_common(bool pack, void* flat, int dtype_flat, const void* const*
   return RP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// topology discovery
+// ---------------------------------------------------------------------------
+
+// NVML, loaded at run time (no link-time dependency): NVLink P2P status of a pair.
+// Returns 1 (NVLink P2P), 0 (no NVLink between them) or -1 (NVML unavailable).
+static int nvml_nvlink_p2p(int dev_a, int dev_b, std::string* why) {
+  static std::mutex mu;
+  static void* h = nullptr;
+  static bool tried = false;
+  typedef nvmlReturn_t (*init_t)(void);
+  typedef nvmlReturn_t (*by_pci_t)(const char*, nvmlDevice_t*);
+  typedef nvmlReturn_t (*p2p_t)(nvmlDevice_t, nvmlDevice_t, nvmlGpuP2PCapsIndex_t, nvmlGpuP2PStatus_t*);
+  static by_pci_t by_pci = nullptr;
+  static p2p_t p2p = nullptr;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!tried) {
+      tried = true;
+      h = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+      if (h) {
+        init_t init = (init_t)dlsym(h, "nvmlInit_v2");
+        by_pci = (by_pci_t)dlsym(h, "nvmlDeviceGetHandleByPciBusId_v2");
+        p2p = (p2p_t)dlsym(h, "nvmlDeviceGetP2PStatus");
+        if (!init || !by_pci || !p2p || init() != NVML_SUCCESS) by_pci = nullptr;
+      }
+    }
+  }
+  if (!by_pci || !p2p) {
+    *why = "NVML unavailable: cannot confirm NVLink";
+    return -1;
+  }
+  char bus_a[32], bus_b[32];
+  nvmlDevice_t na, nb;
+  if (cudaDeviceGetPCIBusId(bus_a, sizeof(bus_a), dev_a) != cudaSuccess ||
+      cudaDeviceGetPCIBusId(bus_b, sizeof(bus_b), dev_b) != cudaSuccess || by_pci(bus_a, &na) != NVML_SUCCESS ||
+      by_pci(bus_b, &nb) != NVML_SUCCESS) {
+    *why = "NVML cannot resolve the devices";
+    return -1;
+  }
+  nvmlGpuP2PStatus_t st = NVML_P2P_STATUS_UNKNOWN;
+  if (p2p(na, nb, NVML_P2P_CAPS_INDEX_NVLINK, &st) != NVML_SUCCESS) {
+    *why = "nvmlDeviceGetP2PStatus failed";
+    return -1;
+  }
+  if (st != NVML_P2P_STATUS_OK) *why = "NVML reports no NVLink P2P (status " + std::to_string((int)st) + ")";
+  return st == NVML_P2P_STATUS_OK ? 1 : 0;
+}
+
+// Link from this rank to peer `me_or_peer` (include/rp.h RP_LINK_*).
+int rp_classify_link(rp_comm* c, const RpExport& me, const RpExport& peer, bool self, std::string* why) {
+  if (self) return RP_LINK_SELF;
+  if (memcmp(peer.uuid, me.uuid, 16) == 0) {
+    if (peer.pid == me.pid && peer.loopback && me.loopback) return RP_LINK_LOOPBACK;
+    *why = "shares this rank's GPU (use a virtual communicator, or a loopback world in one process)";
+    return RP_LINK_SAME_DEVICE;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
+  for (int d = 0; d < ndev; ++d) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) != cudaSuccess) continue;
+    if (memcmp(&prop.uuid, peer.uuid, 16) != 0) continue;
+    int ok = 0, acc = 0;
+    cudaDeviceCanAccessPeer(&ok, c->device, d);
+    cudaDeviceGetP2PAttribute(&acc, cudaDevP2PAttrAccessSupported, c->device, d);
+    if (!ok || !acc) {
+      *why = "no CUDA peer access to device " + std::to_string(d);
+      return RP_LINK_NONE;
+    }
+    const int nv = nvml_nvlink_p2p(c->device, d, why);
+    if (nv == 1) return RP_LINK_NVLINK;
+    return nv == 0 ? RP_LINK_PCIE : RP_LINK_UNKNOWN;
+  }
+  *why = "peer GPU is not visible to this process (CUDA_VISIBLE_DEVICES?)";
+  return RP_LINK_UNKNOWN;
+}
+
 // ===========================================================================
 // C ABI
 // ===========================================================================
 extern "C" {
+
+int rp_topology_check(int world, int rank, const int* links, int allow_pcie, int loopback) {
+  if (!links || world < 1 || world > RP_MAX_RANKS || rank < 0 || rank >= world)
+    return rp_fail(RP_ERR_INVALID, "rp_topology_check: bad arguments");
+  static const char* names[] = {"self", "NVLink", "PCIe peer access only", "no peer access", "unknown",
+                                "same device", "loopback"};
+  for (int p = 0; p < world; ++p) {
+    const int l = links[p];
+    bool ok;
+    switch (l) {
+      case RP_LINK_SELF: ok = p == rank; break;
+      case RP_LINK_NVLINK: ok = true; break;
+      case RP_LINK_PCIE: ok = allow_pcie != 0; break;
+      case RP_LINK_LOOPBACK: ok = loopback != 0; break;
+      default: ok = false;
+    }
+    if (!ok) {
+      const char* n = (l >= 0 && l <= RP_LINK_LOOPBACK) ? names[l] : "invalid";
+      return rp_fail(RP_ERR_CONFIG, "topology: rank " + std::to_string(rank) + " -> rank " + std::to_string(p) +
+                                        " link is '" + n +
+                                        "'; an NVLink/NVSwitch all-to-all is required (no fallback; "
+                                        "RP_ALLOW_PCIE=1 accepts PCIe peer access for tests)");
+    }
+  }
+  return RP_OK;
+}
 
 const char* rp_last_error(void) { return g_last_error.c_str(); }
 
@@ -213,12 +329,14 @@ static int init_device(rp_comm* c) {
 
 static int alloc_region(rp_comm* c, int r) {
   char* base = nullptr;
+  if (!c->aux) RP_CUDA_CHECK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   RP_CUDA_CHECK(cudaMalloc(&base, RP_SIGNAL_BYTES + c->pool_bytes));
-  RP_CUDA_CHECK(cudaMemset(base, 0, RP_SIGNAL_BYTES));
   c->alloc[r] = base;
   c->table.sig[r] = (uint32_t*)base;
   c->table.data[r] = base + RP_SIGNAL_BYTES;
-  RP_CUDA_CHECK(cudaMemset(c->table.data[r] + c->tile_flags(), 0, RP_FLAG_BYTES));
+  RP_CUDA_CHECK(cudaMemsetAsync(base, 0, RP_SIGNAL_BYTES, c->aux));
+  RP_CUDA_CHECK(cudaMemsetAsync(c->table.data[r] + c->tile_flags(), 0, RP_FLAG_BYTES, c->aux));
+  RP_CUDA_CHECK(cudaStreamSynchronize(c->aux));
   return RP_OK;
 }
 
@@ -262,6 +380,7 @@ int rp_comm_create_virtual(int world, int device, size_t pool_bytes, rp_comm_t* 
   if (rc) {
     for (int r = 0; r < world; ++r)
       if (c->alloc[r]) cudaFree(c->alloc[r]);
+    if (c->aux) cudaStreamDestroy(c->aux);
     delete c;
     return rc;
   }
@@ -290,9 +409,33 @@ int rp_comm_export(rp_comm_t c, void* buf, size_t* len) {
   e.pci_bus = prop.pciBusID;
   e.pci_device = prop.pciDeviceID;
   e.pci_domain = prop.pciDomainID;
+  e.base = (uint64_t)(uintptr_t)c->alloc[c->rank];
+  e.pid = (int32_t)getpid();
+  e.loopback = c->loopback ? 1 : 0;
   memcpy(buf, &e, sizeof(e));
   *len = sizeof(e);
   return RP_OK;
+}
+
+// Loopback regions are plain pointers shared by the ranks of one process, so a
+// region may be freed only once EVERY rank that mapped it has destroyed its
+// communicator: a rank that finished (or failed) early must not free memory a
+// peer's kernel may still store into (that was an illegal-address fault).
+static std::mutex g_lb_mu;
+static std::map<char*, int> g_lb_refs;
+
+static void lb_ref(char* base) {
+  std::lock_guard<std::mutex> g(g_lb_mu);
+  ++g_lb_refs[base];
+}
+// Drop one reference; true when the caller must free the region.
+static bool lb_unref(char* base) {
+  std::lock_guard<std::mutex> g(g_lb_mu);
+  auto it = g_lb_refs.find(base);
+  if (it == g_lb_refs.end()) return false;
+  if (--it->second > 0) return false;
+  g_lb_refs.erase(it);
+  return true;
 }
 
 int rp_comm_import(rp_comm_t c, const void* all, size_t len) {
@@ -302,45 +445,80 @@ int rp_comm_import(rp_comm_t c, const void* all, size_t len) {
     return rp_fail(RP_ERR_PROTOCOL, "rp_comm_import: expected world export blobs");
   RP_CUDA_CHECK(cudaSetDevice(c->device));
   const RpExport* ex = (const RpExport*)all;
-  // topology: map peer UUIDs to local ordinals (when visible) and require P2P
-  int ndev = 0;
-  RP_CUDA_CHECK(cudaGetDeviceCount(&ndev));
   for (int p = 0; p < c->world; ++p) {
     if (ex[p].magic != kMagic || ex[p].rank != p || ex[p].world != c->world)
       return rp_fail(RP_ERR_PROTOCOL, "rp_comm_import: blob " + std::to_string(p) + " is not rank " +
                                           std::to_string(p) + " of this world");
     if (ex[p].pool_bytes != c->pool_bytes)
       return rp_fail(RP_ERR_PROTOCOL, "rp_comm_import: ranks disagree on pool_bytes");
-    if (p == c->rank) continue;
-    if (memcmp(ex[p].uuid, ex[c->rank].uuid, 16) == 0)
-      return rp_fail(RP_ERR_CONFIG, "ranks " + std::to_string(c->rank) + " and " + std::to_string(p) +
-                                        " share one GPU; use a virtual communicator for replicas on one device");
-    for (int d = 0; d < ndev; ++d) {
-      cudaDeviceProp prop;
-      if (cudaGetDeviceProperties(&prop, d) != cudaSuccess) continue;
-      if (memcmp(&prop.uuid, ex[p].uuid, 16) != 0) continue;
-      int ok = 0;
-      RP_CUDA_CHECK(cudaDeviceCanAccessPeer(&ok, c->device, d));
-      int acc = 0;
-      cudaDeviceGetP2PAttribute(&acc, cudaDevP2PAttrAccessSupported, c->device, d);
-      if (!ok || !acc)
-        return rp_fail(RP_ERR_CONFIG, "no peer access between device " + std::to_string(c->device) +
-                                          " and device " + std::to_string(d) +
-                                          " (NVLink/NVSwitch all-to-all required; no fallback)");
-    }
+    if (ex[p].loopback != (c->loopback ? 1 : 0))
+      return rp_fail(RP_ERR_PROTOCOL, "rp_comm_import: ranks disagree on loopback mode");
+  }
+  // topology discovered at init: classify the link to every peer, then apply the
+  // policy (rp_topology_check) -- NVLink P2P to every peer, or a loopback world
+  int links[RP_MAX_RANKS];
+  std::string why[RP_MAX_RANKS];
+  for (int p = 0; p < c->world; ++p) links[p] = rp_classify_link(c, ex[c->rank], ex[p], p == c->rank, &why[p]);
+  const char* pe = getenv("RP_ALLOW_PCIE");
+  const int allow = (pe && pe[0] == '1') ? 1 : 0;
+  int rc = rp_topology_check(c->world, c->rank, links, allow, c->loopback ? 1 : 0);
+  if (rc) {
+    for (int p = 0; p < c->world; ++p)
+      if (!why[p].empty()) rp_set_error(rp_last_error() + std::string("; rank ") + std::to_string(p) + ": " + why[p]);
+    return rc;
+  }
+  if (c->loopback) {
+    for (int p = 0; p < c->world; ++p) lb_ref(p == c->rank ? c->alloc[c->rank] : (char*)(uintptr_t)ex[p].base);
+    c->lb_refs = true;
   }
   for (int p = 0; p < c->world; ++p) {
     if (p == c->rank) continue;
-    void* ptr = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&ptr, ex[p].handle, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess)
-      return rp_fail(RP_ERR_CONFIG, "cudaIpcOpenMemHandle(rank " + std::to_string(p) + "): " + cudaGetErrorString(e));
-    c->ipc_opened[p] = true;
-    c->alloc[p] = (char*)ptr;
+    char* ptr = nullptr;
+    if (links[p] == RP_LINK_LOOPBACK) {
+      ptr = (char*)(uintptr_t)ex[p].base;  // same process, same device: a plain pointer (not owned)
+    } else {
+      void* vp = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&vp, ex[p].handle, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess)
+        return rp_fail(RP_ERR_CONFIG, "cudaIpcOpenMemHandle(rank " + std::to_string(p) + "): " + cudaGetErrorString(e));
+      c->ipc_opened[p] = true;
+      c->alloc[p] = (char*)vp;
+      ptr = (char*)vp;
+    }
     c->table.sig[p] = (uint32_t*)ptr;
-    c->table.data[p] = (char*)ptr + RP_SIGNAL_BYTES;
+    c->table.data[p] = ptr + RP_SIGNAL_BYTES;
   }
   c->imported = true;
+  return RP_OK;
+}
+
+int rp_loopback_prepare(int device) {
+  // The stream-ordered allocator may hand one rank's stream memory another rank's
+  // stream freed, inserting a wait on that stream (internal dependency). In a
+  // loopback world that wait can close a cycle -- stream A waits for B's free
+  // point, queued behind B's collective kernel, which waits for A's next kernel --
+  // so cross-stream reuse is limited to frees that already completed
+  // (opportunistic) or that the caller ordered (event dependencies).
+  RP_CUDA_CHECK(cudaSetDevice(device));
+  cudaMemPool_t pools[2] = {nullptr, nullptr};
+  RP_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pools[0], device));
+  RP_CUDA_CHECK(cudaDeviceGetMemPool(&pools[1], device));
+  for (cudaMemPool_t p : pools) {
+    int off = 0;
+    RP_CUDA_CHECK(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &off));
+  }
+  return RP_OK;
+}
+
+int rp_comm_set_loopback(rp_comm_t c, int on) {
+  if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_set_loopback: NULL comm");
+  if (c->is_virtual) return rp_fail(RP_ERR_INVALID, "rp_comm_set_loopback: virtual communicators are already local");
+  if (c->imported && c->world > 1) return rp_fail(RP_ERR_INVALID, "rp_comm_set_loopback: call before rp_comm_import");
+  c->loopback = on != 0;
+  // every rank's blocks must be co-resident with every other rank's: at most
+  // num_sms / world blocks per rank, each at most one SM, so an empty SM always
+  // exists while any block of the world is still unscheduled
+  c->loopback_cap = c->loopback ? std::max(1, c->num_sms / c->world) : 0;
   return RP_OK;
 }
 
@@ -349,12 +527,22 @@ int rp_comm_destroy(rp_comm_t c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   rp_nvls_destroy(c);
-  for (int r = 0; r < RP_MAX_RANKS; ++r) {
-    if (!c->alloc[r]) continue;
-    if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->alloc[r]);
-    else cudaFree(c->alloc[r]);
+  if (c->lb_refs) {
+    // every rank's region, freed by whichever rank lets go of it last
+    for (int r = 0; r < c->world; ++r) {
+      char* base = (char*)c->table.sig[r];
+      if (base && lb_unref(base)) cudaFree(base);
+    }
+  } else {
+    for (int r = 0; r < RP_MAX_RANKS; ++r) {
+      if (!c->alloc[r]) continue;
+      if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->alloc[r]);
+      else if (r == c->rank || c->is_virtual) cudaFree(c->alloc[r]);
+    }
   }
+  if (c->aux) cudaStreamDestroy(c->aux);
   if (c->bn_partials) cudaFree(c->bn_partials);
+  for (double* p : c->bn_retired) cudaFree(p);
   delete c;
   return RP_OK;
 }
@@ -402,16 +590,31 @@ int rp_comm_set_block_cap(rp_comm_t c, int blocks) {
 int rp_comm_check(rp_comm_t c) {
   if (!c) return rp_fail(RP_ERR_INVALID, "rp_comm_check: NULL comm");
   RP_CUDA_CHECK(cudaSetDevice(c->device));
-  RP_CUDA_CHECK(cudaDeviceSynchronize());
-  uint32_t worst = 0;
+  // a loopback world shares the device with its peers: a device-wide sync could
+  // wait on a peer kernel that waits for this rank's next launch; the caller syncs
+  // the streams it launched on instead
+  if (!c->loopback) RP_CUDA_CHECK(cudaDeviceSynchronize());
+  uint32_t worst = 0, info[3] = {0, 0, 0};
   for (int r = 0; r < c->world; ++r) {
     if (!c->is_virtual && r != c->rank) continue;
-    uint32_t w = 0;
-    RP_CUDA_CHECK(cudaMemcpy(&w, c->table.sig[r] + RP_ABORT_WORD, 4, cudaMemcpyDeviceToHost));
-    worst = std::max(worst, w);
+    uint32_t w[4] = {0, 0, 0, 0};
+    RP_CUDA_CHECK(cudaMemcpyAsync(w, c->table.sig[r] + RP_ABORT_WORD, 16, cudaMemcpyDeviceToHost, c->aux));
+    RP_CUDA_CHECK(cudaStreamSynchronize(c->aux));
+    if (w[0] > worst || (w[0] == RP_ABORT_TIMEOUT && worst != RP_ABORT_TIMEOUT)) {
+      worst = w[0];
+      memcpy(info, w + 1, sizeof(info));
+    }
   }
-  if (worst == RP_ABORT_TIMEOUT)
-    return rp_fail(RP_ERR_ABORTED, "collective timed out waiting for a peer (dead or diverged rank)");
+  if (worst == RP_ABORT_TIMEOUT) {
+    // which signal word the wait was on: row (block index / BN row / phase row) and source rank
+    const uint32_t row = info[0] / RP_MAX_RANKS, src = info[0] % RP_MAX_RANKS;
+    std::string where = row >= (uint32_t)RP_PH_ROW0 && row < (uint32_t)RP_CTR_ROW
+                            ? "phase row " + std::to_string(row - RP_PH_ROW0)
+                            : (row >= (uint32_t)RP_BN_ROW0 ? "BN row " : "block row ") + std::to_string(row);
+    return rp_fail(RP_ERR_ABORTED, "collective timed out waiting for a peer (dead or diverged rank): " + where +
+                                       ", source rank " + std::to_string(src) + ", waited for " +
+                                       std::to_string(info[1]) + ", saw " + std::to_string(info[2]));
+  }
   if (worst == RP_ABORT_PEER) return rp_fail(RP_ERR_ABORTED, "collective aborted by another rank");
   return RP_OK;
 }

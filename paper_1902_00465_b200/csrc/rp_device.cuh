@@ -86,8 +86,13 @@ __device__ __forceinline__ bool wait_reach(const RankTable& t, int world, uint64
       const uint64_t now = globaltimer();
       if (t0 == 0) t0 = now;
       else if (now - t0 > timeout_ns) {
-        // record the timeout locally and tell every peer to stop waiting
-        atomicCAS(abort_word, 0u, RP_ABORT_TIMEOUT);
+        // record the timeout locally (with the word, target and value seen, for
+        // rp_comm_check's message) and tell every peer to stop waiting
+        if (atomicCAS(abort_word, 0u, RP_ABORT_TIMEOUT) == 0u) {
+          abort_word[1] = (uint32_t)(p - t.sig[rank]);
+          abort_word[2] = target;
+          abort_word[3] = ld_relaxed_sys(p);
+        }
         for (int q = 0; q < world; ++q)
           if (q != rank) atomicCAS(t.sig[q] + RP_ABORT_WORD, 0u, RP_ABORT_PEER);
         return false;
@@ -95,6 +100,13 @@ __device__ __forceinline__ bool wait_reach(const RankTable& t, int world, uint64
     }
   }
   return true;
+}
+
+// A communicator that aborted stays aborted (rp_comm_check): every later kernel
+// returns at once, so nothing is stored into a peer's pool after an abort (in a
+// loopback world a peer that gave up may be tearing its region down).
+__device__ __forceinline__ bool rp_aborted(const RankTable& t, int rank) {
+  return ld_relaxed_sys(t.sig[rank] + RP_ABORT_WORD) != 0u;
 }
 
 __device__ __forceinline__ bool rank_barrier(const RankTable& t, int world, uint64_t timeout_ns, int rank,

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/rp.h"
 
@@ -87,10 +88,28 @@ struct rp_comm {
   int num_sms = 148;
   int max_coresident = 0;
   int block_cap = 0;       // >0: at most this many blocks per rank (rp_comm_set_block_cap)
+  // loopback world (rp_comm_set_loopback): several non-virtual ranks in ONE process
+  // on ONE device, each driven from its own host thread and stream. Peers' regions
+  // are plain pointers of this process (no IPC), and every rank's grids are capped
+  // at num_sms / world blocks so all ranks' blocks are co-resident.
+  bool loopback = false;
+  int loopback_cap = 0;    // num_sms / world in a loopback world
+  bool lb_refs = false;    // holds a reference on every rank's region (loopback registry)
+  // effective per-rank block cap (0: none): the caller's cap and the loopback cap
+  int cap() const {
+    if (loopback_cap > 0) return block_cap > 0 ? (block_cap < loopback_cap ? block_cap : loopback_cap) : loopback_cap;
+    return block_cap;
+  }
   // BN scratch: per-split f64 partials (device memory, all local replicas)
   double* bn_partials = nullptr;
   size_t bn_partials_bytes = 0;
+  std::vector<double*> bn_retired;  // outgrown partials, freed with the communicator
   void* nvls = nullptr;    // NvlsState (rp_nvls.cu): multicast-bound region, or NULL
+  // private non-blocking stream for the library's own small copies (signal-region
+  // init, rp_comm_check's abort read): never the legacy default stream, which
+  // waits for every blocking stream -- in a loopback world, for a peer's kernel
+  // that waits for this rank (measured: a 5 s stall until the spin timeout)
+  cudaStream_t aux = nullptr;
   // end of the general staging window (see the layout above)
   size_t scratch_end() const { return pool_bytes - RP_BN_BYTES - RP_FLAG_BYTES - 2 * RP_OS_REGION; }
   size_t oneshot_zone(int parity) const { return scratch_end() + (size_t)parity * RP_OS_REGION; }
@@ -106,6 +125,9 @@ struct RpExport {
   cudaIpcMemHandle_t handle;
   unsigned char uuid[16];
   int32_t pci_bus, pci_device, pci_domain;
+  uint64_t base;     // region base in the exporting process (loopback peers only)
+  int32_t pid;       // exporting process
+  int32_t loopback;  // exporter runs a loopback world
 };
 
 // Kernel argument block for the collectives (by value, < 4 KB).
@@ -128,6 +150,8 @@ struct CollArgs {
   uint32_t tile_v;            // dynamically scheduled kernels: vectors (16 B) per tile
   int relay_root_blocks;      // relay broadcast: blocks the root pushes with
 };
+
+int rp_classify_link(rp_comm* c, const RpExport& me, const RpExport& peer, bool self, std::string* why);
 
 // error plumbing
 void rp_set_error(const std::string& msg);
@@ -167,6 +191,9 @@ int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, 
               cudaStream_t stream);
 // Blocks per rank for a collective kernel given its per-block occupancy.
 int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want);
+// Co-resident block budget per rank for kernels that size their own grid (BN):
+// occupancy x SMs, divided among virtual replicas, and at most the block cap.
+int64_t rp_wave_per_rank(rp_comm* c, int per_sm);
 
 // shared collective plumbing (rp_collectives.cu), used by rp_apply.cu. The
 // dynamically scheduled launch passes &a as the kernel's only parameter: a kernel

@@ -374,6 +374,7 @@ template <int DT, int OP>
 __global__ void __launch_bounds__(kNvlsThreads) ar_nvls(const CollArgs a) {
   using T = typename DType<DT>::T;
   const int rank = a.rank;
+  if (rp_aborted(a.t, rank)) return;
   char* mc = (char*)a.src[rank];  // the multicast view of this message
   const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
   const size_t Vc = a.chunk;
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(kNvlsThreads) ar_nvls(const CollArgs a) {
 template <bool ROOT_UNUSED = false>
 __global__ void __launch_bounds__(kNvlsThreads) bcast_nvls(const CollArgs a) {
   const int rank = a.rank;
+  if (rp_aborted(a.t, rank)) return;
   char* mc = (char*)a.dst[rank];  // multicast view of the destination
   const char* src = (const char*)a.src[rank];
   const size_t V = a.count / 16;
@@ -552,6 +554,7 @@ template <int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) bcast_relay(const CollArgs a) {
   constexpr int kU = MINB > 1 ? 4 : 8;  // 16-byte vectors in flight per thread
   const int rank = a.rank, W = a.world, root = a.root;
+  if (rp_aborted(a.t, rank)) return;
   const size_t B = a.count;
   const size_t tb = (size_t)a.tile_v * 16;
   const uint32_t nt = (uint32_t)((B + tb - 1) / tb);

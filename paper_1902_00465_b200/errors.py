@@ -18,6 +18,13 @@ class ShapeError(GraphError):
     """Operand shapes / dtypes invalid for an op (errors.py:12)."""
 
 
+class NotDifferentiableError(GraphError):
+    """Backpropagation reached an op without a VJP (errors.py:16): here a collective
+    on in-process virtual replicas, whose backward passes share one autograd device
+    thread and so cannot rendezvous (the reference raises it for every collective,
+    graph.py:798-800)."""
+
+
 class EvaluationError(GraphError):
     """Runtime failure while executing (errors.py:24)."""
 

@@ -98,7 +98,7 @@ class _Group:
         self.grads.pack()
         lib = _lib.load()
         hyper = (ctypes.c_double * 6)(*_hyper(self.code, group))
-        stream = torch.cuda.current_stream(self.pflat[0].device).cuda_stream
+        stream = self.comm._stream()
         gcode = dtype_code(self.grads.comm_dtype)
         n = self.grads.numel
         s1 = [t.data_ptr() if t is not None else 0 for t in self.state1]

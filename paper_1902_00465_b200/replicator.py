@@ -134,8 +134,13 @@ class _Rendezvous:
 
 
 # ---------------------------------------------------------------------------
-# differentiable collectives (multi-process). The reference has no VJP for its
-# collectives (graph.py:562, :585); all_sum's adjoint is all_sum.
+# differentiable collectives. The reference has no VJP for its collectives and
+# raises NotDifferentiableError when backprop reaches one (graph.py:798-800).
+# Multi-process replicas implement the adjoints (all_sum's adjoint is all_sum;
+# all_gather's is a reduce-scatter; broadcast's sums every rank's cotangent into
+# the root); in-process virtual replicas keep the reference's error, raised at
+# backward time, because their backward passes run on ONE autograd device thread
+# and cannot rendezvous.
 # ---------------------------------------------------------------------------
 
 class _AllReduceFn(torch.autograd.Function):
@@ -147,9 +152,57 @@ class _AllReduceFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         if ctx.kind == "max":
-            raise errors.ShapeError("all_reduce(max) is not differentiable")
+            raise errors.NotDifferentiableError("all_reduce(max) has no VJP (graph.py:798-800)")
         # y = sum_r w*x_r (w = 1 or 1/N): dL/dx_r = w * sum_q dL_q/dy_q
         return ctx.comm.all_reduce_tensor(g.contiguous(), ctx.kind), None, None
+
+
+class _AllGatherFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, comm):
+        ctx.comm = comm
+        return comm.all_gather_tensor(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        # y_q[r] = x_r on every rank q: dL/dx_r = sum_q dL_q/dy_q[r]
+        return ctx.comm.all_reduce_tensor(g.contiguous(), "sum")[ctx.comm.rank], None
+
+
+class _BroadcastFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, comm, root):
+        ctx.comm, ctx.root = comm, root
+        return comm.broadcast_tensor(x.detach().clone(), root=root)
+
+    @staticmethod
+    def backward(ctx, g):
+        # every rank's output is root's x: root's x collects every rank's cotangent
+        total = ctx.comm.all_reduce_tensor(g.contiguous(), "sum")
+        return (total if ctx.comm.rank == ctx.root else torch.zeros_like(g)), None, None
+
+
+class _NoVJP(torch.autograd.Function):
+    """Identity in the forward; backward raises NotDifferentiableError naming the
+    collective (virtual replicas, graph.py:798-800)."""
+
+    @staticmethod
+    def forward(ctx, x, y, what):
+        ctx.what = what
+        return y.view_as(y)
+
+    @staticmethod
+    def backward(ctx, g):
+        raise errors.NotDifferentiableError(
+            f"backprop reached {ctx.what} on in-process virtual replicas, which have no VJP (graph.py:798-800); "
+            "use one process per GPU (torch.distributed or a loopback world) to differentiate collectives")
+
+
+def _novjp(x, y, what):
+    """Attach a raising backward to y when autograd would flow through x."""
+    if torch.is_grad_enabled() and isinstance(x, torch.Tensor) and x.requires_grad:
+        return _NoVJP.apply(x, y, what)
+    return y
 
 
 # ---------------------------------------------------------------------------
@@ -182,7 +235,7 @@ class Replicator:
     def __init__(self, num_replicas: int | None = None, *, group=None, device: int | None = None,
                  pool_bytes: int = DEFAULT_POOL_BYTES, timeout_s: float = 20.0,
                  grad_comm_dtype: torch.dtype | None = None, bucket_bytes: int | None = None,
-                 nvls_bytes: int = 0, check_protocol: bool = False, grad_views: bool = True):
+                 nvls_bytes: int = 0, check_protocol: bool = False, grad_views: bool = True, bootstrap=None):
         """``nvls_bytes`` > 0 (multi-process, >= 2 ranks): bind that much memory per
         rank to an NVSwitch multicast region and place gradient fusion buckets in it
         while it has room, so wrap_optimizer's reduction runs in the switch
@@ -196,18 +249,26 @@ class Replicator:
         checks that all ranks issue the same (generation, call index, label, kind,
         shape, dtype) and that no label repeats within a generation (one
         generation per ``run``/``new_generation``), raising ProtocolError naming the
-        ranks. Virtual replicas are always checked by the rendezvous."""
+        ranks. Virtual replicas are always checked by the rendezvous.
+
+        ``bootstrap`` (bootstrap.py): the ranks' rendezvous -- default the
+        initialised torch.distributed group; ``LoopbackWorld.bootstrap(rank)`` runs
+        one-replica-per-rank communicators in one process on one GPU."""
         import torch.distributed as dist
 
-        mp = dist.is_available() and dist.is_initialized()
-        if mp:
-            if num_replicas not in (None, dist.get_world_size(group)):
+        from .bootstrap import DistBootstrap
+
+        if bootstrap is None and dist.is_available() and dist.is_initialized():
+            bootstrap = DistBootstrap(group)
+        if bootstrap is not None:
+            if num_replicas not in (None, bootstrap.world):
                 raise errors.ConfigurationError("num_replicas must equal the process-group size")
-            self.comm = Communicator(group=group, device=device, pool_bytes=pool_bytes, timeout_s=timeout_s)
+            self.comm = Communicator(device=device, pool_bytes=pool_bytes, timeout_s=timeout_s,
+                                     bootstrap=bootstrap)
             self.kind = "multi_gpu" if self.comm.world > 1 else "non"
             self._rv = None
             if nvls_bytes > 0 and self.comm.world > 1:
-                self.comm.enable_nvls(int(nvls_bytes), group=group)
+                self.comm.enable_nvls(int(nvls_bytes))
         else:
             n = 1 if num_replicas is None else int(num_replicas)
             if n < 1 or n > 8:
@@ -387,8 +448,9 @@ class Replicator:
         if self.comm.world == 1:
             return _AllReduceFn.apply(x, self.comm, kind) if not self.is_virtual else x.clone()
         if self.is_virtual:
-            return self._collective(("all_reduce", label, kind, tuple(x.shape), x.dtype), x,
-                                    lambda xs: self.comm.all_reduce(xs, kind))
+            y = self._collective(("all_reduce", label, kind, tuple(x.shape), x.dtype), x.detach(),
+                                 lambda xs: self.comm.all_reduce(xs, kind))
+            return _novjp(x, y, f"all_reduce({kind})")
         self._verify(label, kind, x.shape, x.dtype)
         return _AllReduceFn.apply(x, self.comm, kind)
 
@@ -403,23 +465,28 @@ class Replicator:
             if self.comm.world == 1:
                 return [x.clone()] if ragged else x.unsqueeze(0).clone()
             if ragged:
-                return self._collective(("all_gather_ragged", label, tuple(x.shape[1:]), x.dtype), x,
-                                        lambda xs: self.comm.all_gather_ragged(xs))
-            return self._collective(("all_gather", label, tuple(x.shape), x.dtype), x,
-                                    lambda xs: self.comm.all_gather(xs))
+                parts = self._collective(("all_gather_ragged", label, tuple(x.shape[1:]), x.dtype), x.detach(),
+                                         lambda xs: self.comm.all_gather_ragged(xs))
+                return [_novjp(x, t, "all_gather") for t in parts]
+            y = self._collective(("all_gather", label, tuple(x.shape), x.dtype), x.detach(),
+                                 lambda xs: self.comm.all_gather(xs))
+            return _novjp(x, y, "all_gather")
         self._verify(label, "gather", x.shape[1:] if ragged else x.shape, x.dtype)
         if ragged:
+            if torch.is_grad_enabled() and x.requires_grad:
+                raise errors.NotDifferentiableError("ragged all_gather has no VJP; gather x.detach()")
             return self.comm.all_gather_ragged(x)
-        return self.comm.all_gather_tensor(x)
+        return _AllGatherFn.apply(x, self.comm)
 
     def broadcast(self, x: torch.Tensor, root: int = 0, label: str | None = None) -> torch.Tensor:
         if self.is_virtual:
             if self.comm.world == 1:
                 return x.clone()
-            return self._collective(("broadcast", label, root, tuple(x.shape), x.dtype), x,
-                                    lambda xs: self.comm.broadcast(xs, root=root))
+            y = self._collective(("broadcast", label, root, tuple(x.shape), x.dtype), x.detach(),
+                                 lambda xs: self.comm.broadcast(xs, root=root))
+            return _novjp(x, y, "broadcast")
         self._verify(label, f"broadcast(root={root})", x.shape, x.dtype)
-        return self.comm.broadcast_tensor(x.clone(), root=root)
+        return _BroadcastFn.apply(x, self.comm, root)
 
     def map_gather(self, x: torch.Tensor, label: str | None = None) -> "DriverValue":
         """per-replica values collected to the driver; replicas get
@@ -522,9 +589,11 @@ class ReplicatedOptimizer:
 # ---------------------------------------------------------------------------
 
 def _bn_layout(x: torch.Tensor):
-    """(layout, rows, C, hw) for x of shape [N, C] or [N, C, *spatial]."""
+    """(layout, rows, C, hw) for a DENSE x of shape [N, C] or [N, C, *spatial] that
+    the kernels can read as stored; None for any other strides (stride-0 expands,
+    transposes, slices), which the caller makes dense first."""
     if x.dim() == 2:
-        return _lib.NHWC, x.shape[0], x.shape[1], 1
+        return (_lib.NHWC, x.shape[0], x.shape[1], 1) if x.is_contiguous() else None
     n, c = x.shape[0], x.shape[1]
     hw = 1
     for s in x.shape[2:]:
@@ -538,6 +607,15 @@ def _bn_layout(x: torch.Tensor):
     return None
 
 
+def _like_layout(t: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    """t made dense in the memory format the kernels read x in (x already dense)."""
+    if x.dim() == 4 and not x.is_contiguous() and x.is_contiguous(memory_format=torch.channels_last):
+        return t.contiguous(memory_format=torch.channels_last)
+    if x.dim() == 5 and not x.is_contiguous() and x.is_contiguous(memory_format=torch.channels_last_3d):
+        return t.contiguous(memory_format=torch.channels_last_3d)
+    return t.contiguous()
+
+
 def _bn_stats(comm, xs, eps):
     """K5 over the local replicas' inputs ``xs`` (one tensor per local replica).
     Returns per-replica (mean, var, invstd, count) on the device."""
@@ -545,7 +623,7 @@ def _bn_stats(comm, xs, eps):
     x0 = xs[0]
     layout, rows, c, hw = _bn_layout(x0)
     dev = x0.device
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    stream = comm._stream()
     outs = [(torch.empty(c, dtype=torch.float32, device=dev), torch.empty(c, dtype=torch.float32, device=dev),
              torch.empty(c, dtype=torch.float32, device=dev), torch.empty(1, dtype=torch.float64, device=dev))
             for _ in xs]
@@ -616,15 +694,15 @@ class _CrossReplicaBNFn(torch.autograd.Function):
         if not training:
             raise errors.ShapeError("cross-replica BN backward in eval mode is not supported")
         if isinstance(comm, VirtualCommunicator) and comm.world > 1:
-            raise errors.ConfigurationError(
-                "cross-replica BN backward needs one process per GPU; in-process virtual replicas support "
-                "the forward statistics only (as the reference, whose collectives have no VJP, graph.py:562)")
+            raise errors.NotDifferentiableError(
+                "cross-replica BN backward needs one process per GPU (or a loopback world); in-process virtual "
+                "replicas support the forward statistics only (as the reference, whose collectives have no VJP, "
+                "graph.py:798-800)")
         if _bn_layout(dy) != (layout, rows, c, hw):
-            dy = dy.contiguous(memory_format=torch.channels_last) if (layout == _lib.NHWC and x.dim() == 4) \
-                else dy.contiguous()
+            dy = _like_layout(dy, x)
         lib = _lib.load()
         dev = x.device
-        stream = torch.cuda.current_stream(dev).cuda_stream
+        stream = comm._stream()
         code = dtype_code(x.dtype)
         sum_dy = torch.empty(c, dtype=torch.float32, device=dev)
         sum_dy_xmu = torch.empty_like(sum_dy)
@@ -639,10 +717,12 @@ class _CrossReplicaBNFn(torch.autograd.Function):
         _lib.check(lib.rp_bn_bwd_stats(comm._handle, ptrs[0], ptrs[1], code, rows, c, hw, layout, *ptrs[2:], stream),
                    "bn_bwd_stats")
         dx = torch.empty_like(x)
-        m_total = float(count.item()) if count is not None else float(rows * hw * comm.world)
+        # the global count M stays on the device (no host sync per backward)
+        m_total = float(rows * hw * comm.world)
         _lib.check(lib.rp_bn_bwd_apply(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), code, rows, c, hw, layout,
                                        mean.data_ptr(), invstd.data_ptr(), w.data_ptr() if has_w else None,
-                                       sum_dy.data_ptr(), sum_dy_xmu.data_ptr(), m_total, stream), "bn_bwd_apply")
+                                       sum_dy.data_ptr(), sum_dy_xmu.data_ptr(), m_total,
+                                       count.data_ptr() if count is not None else None, stream), "bn_bwd_apply")
         dw = (loc_dy_xmu * invstd).to(wdt) if has_w else None
         db = loc_dy.to(wdt) if has_b else None
         return dx, dw, db, None, None, None, None, None, None

@@ -391,7 +391,14 @@ def test_bn_apply_kernels_match_torch():
         dx = torch.empty_like(xx)
         _lib.check(lib.rp_bn_bwd_apply(xx.data_ptr(), dd.data_ptr(), dx.data_ptr(), 0, rows, 24, hw, layout,
                                        mean.data_ptr(), invstd.data_ptr(), w.data_ptr(), sdy.data_ptr(),
-                                       sdyx.data_ptr(), 100.0, s))
+                                       sdyx.data_ptr(), 100.0, None, s))
+        # the same with M read on the device (no host sync, as autograd's backward does)
+        cnt = torch.tensor([100.0], dtype=torch.float64, device=DEV)
+        dx2 = torch.empty_like(xx)
+        _lib.check(lib.rp_bn_bwd_apply(xx.data_ptr(), dd.data_ptr(), dx2.data_ptr(), 0, rows, 24, hw, layout,
+                                       mean.data_ptr(), invstd.data_ptr(), w.data_ptr(), sdy.data_ptr(),
+                                       sdyx.data_ptr(), 0.0, cnt.data_ptr(), s))
+        assert torch.equal(dx, dx2)
         xt = x.clone().requires_grad_(True)
         yt = torch.nn.functional.batch_norm(xt, None, None, w, b, training=True, eps=1e-5)
         yt.backward(dy)
@@ -470,6 +477,28 @@ def test_replicator_paper_batch_norm_kat():
     outs = repl.run(lambda h: repl.batch_norm(h), lambda r: hs[r])
     for r in range(2):
         np.testing.assert_allclose(host(outs[r]), (host(hs[r]) - 4) / np.sqrt(5 + 1e-5), rtol=0, atol=1e-15)
+    repl.comm.close()
+
+
+def test_virtual_collectives_refuse_backprop():
+    """in-process virtual replicas cannot rendezvous in backward (their
+    backward passes share one autograd device thread), so backprop reaching a
+    collective raises the reference's NotDifferentiableError (graph.py:798-800)
+    instead of silently dropping the gradient; the forward values are unchanged,
+    and inputs that do not require grad are unaffected."""
+    repl = Replicator(num_replicas=2, device=0, pool_bytes=16 << 20)
+
+    def step(x):
+        y = repl.all_sum(x, label="s")
+        y.sum().backward()
+
+    with pytest.raises(errors.NotDifferentiableError):
+        repl.run(step, lambda r: torch.full((3,), float(r + 1), device=DEV, requires_grad=True))
+    outs = repl.run(lambda x: repl.all_sum(x * 2, label="t"),
+                    lambda r: torch.full((3,), float(r + 1), device=DEV, requires_grad=True))
+    assert all(host(o.detach()).tolist() == [6.0] * 3 and o.requires_grad for o in outs)
+    outs = repl.run(lambda x: repl.broadcast(x, root=1), lambda r: torch.full((2,), float(r), device=DEV))
+    assert all(host(o).tolist() == [1.0, 1.0] and not o.requires_grad for o in outs)
     repl.comm.close()
 
 

@@ -147,6 +147,18 @@ def test_bn_layout_detection():
     cl = torch.empty(2, 3, 4, 5).contiguous(memory_format=torch.channels_last)
     assert _bn_layout(cl) == (_lib.NHWC, 40, 3, 1)
     assert _bn_layout(torch.empty(2, 3, 4, 5).transpose(2, 3)) is None
+    # non-dense 2-D / 5-D inputs are not read as stored (a stride-0 dy
+    # from .sum().backward() or a transpose must be made dense first)
+    assert _bn_layout(torch.empty(3, 8).t()) is None
+    assert _bn_layout(torch.ones(1).expand(8, 3)) is None
+    assert _bn_layout(torch.empty(8, 6)[:, ::2]) is None
+    c3 = torch.empty(2, 3, 4, 5, 6).contiguous(memory_format=torch.channels_last_3d)
+    assert _bn_layout(c3) == (_lib.NHWC, 240, 3, 1)
+    from paper_1902_00465_b200.replicator import _like_layout
+    assert _like_layout(torch.ones(1).expand(2, 3, 4, 5, 6), c3).stride() == c3.stride()
+    cl4 = torch.empty(2, 3, 4, 5).contiguous(memory_format=torch.channels_last)
+    assert _like_layout(torch.ones(1).expand(2, 3, 4, 5), cl4).stride() == cl4.stride()
+    assert _like_layout(torch.ones(1).expand(8, 3), torch.empty(8, 3)).is_contiguous()
 
 
 # --- world_size 2 over gloo: bootstrap exchange ----------------------------------
@@ -263,3 +275,93 @@ def test_relay_broadcast_tile_partition():
                                 break
                             got.append(i)
                     assert sorted(owned + got) == list(range(nt)), (world, root, nt, rank)
+
+
+# --- topology policy (rp_comm_import, include/rp.h rp_topology_check) -----------
+
+def _links(*kinds):
+    import ctypes
+    arr = (ctypes.c_int * len(kinds))(*kinds)
+    return arr
+
+
+def test_topology_policy_requires_nvlink_everywhere():
+    """An NVSwitch all-to-all (NVLink to every peer) passes; a PCIe-only peer, a
+    peer without peer access, an invisible peer or another process on the same GPU
+    is a ConfigurationError naming the pair (errors.py:32); RP_ALLOW_PCIE
+    admits PCIe for tests, and same-GPU ranks only inside a loopback world."""
+    lib = _lib.load()
+    S, NV, PCIE, NONE, UNK, SAME, LOOP = (_lib.LINK_SELF, _lib.LINK_NVLINK, _lib.LINK_PCIE, _lib.LINK_NONE,
+                                          _lib.LINK_UNKNOWN, _lib.LINK_SAME_DEVICE, _lib.LINK_LOOPBACK)
+    _lib.check(lib.rp_topology_check(4, 1, _links(NV, S, NV, NV), 0, 0))
+    for bad, what in ((PCIE, "PCIe"), (NONE, "no peer access"), (UNK, "unknown"), (SAME, "same device"),
+                      (LOOP, "loopback")):
+        with pytest.raises(errors.ConfigurationError) as ei:
+            _lib.check(lib.rp_topology_check(4, 1, _links(NV, S, bad, NV), 0, 0), "comm_import")
+        assert "rank 1 -> rank 2" in str(ei.value) and what in str(ei.value), str(ei.value)
+    _lib.check(lib.rp_topology_check(2, 0, _links(S, PCIE), 1, 0))      # RP_ALLOW_PCIE=1
+    _lib.check(lib.rp_topology_check(3, 2, _links(LOOP, LOOP, S), 0, 1))  # loopback world
+    with pytest.raises(errors.ConfigurationError):
+        _lib.check(lib.rp_topology_check(2, 0, _links(S, SAME), 1, 1))  # another process on this GPU
+    with pytest.raises(errors.ConfigurationError):
+        _lib.check(lib.rp_topology_check(2, 0, _links(NV, S), 0, 0))    # "self" on the wrong rank
+    with pytest.raises(errors.ShapeError):
+        _lib.check(lib.rp_topology_check(9, 0, _links(*([NV] * 9)), 0, 0))
+
+
+# --- loopback bootstrap (bootstrap.py) ------------------------------------------
+
+def test_loopback_bootstrap_exchanges_in_rank_order():
+    """The in-process rendezvous a loopback world's communicators bootstrap over:
+    all_gather_object returns every rank's object in rank order (repeatedly, no
+    slot reuse race), broadcast_object delivers the root's, and a failing rank
+    breaks the barrier instead of hanging the others."""
+    from paper_1902_00465_b200.bootstrap import LoopbackWorld
+
+    lw = LoopbackWorld(4, device=0, timeout_s=30, allow_native_allocator=True)
+
+    def body(r):
+        b = lw.bootstrap(r)
+        outs = [b.all_gather_object((r, k)) for k in range(20)]
+        return outs, b.broadcast_object(f"root{r}", src=2)
+
+    def run():
+        import threading as th
+        res = [None] * 4
+
+        def w(r):
+            res[r] = body(r)
+        ts = [th.Thread(target=w, args=(r,)) for r in range(4)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=60)
+        return res
+    res = run()
+    for r in range(4):
+        outs, root = res[r]
+        assert outs == [[(q, k) for q in range(4)] for k in range(20)]
+        assert root == "root2"
+
+    lw2 = LoopbackWorld(3, device=0, timeout_s=30, allow_native_allocator=True)
+
+    def failing(r):
+        if r == 1:
+            raise ValueError("rank 1 fails before the rendezvous")
+        lw2.bootstrap(r).barrier()
+
+    errs = _run_threads(3, lambda r: failing(r) if r != 1 else (lw2._barrier.abort(), failing(r)))[1]
+    assert isinstance(errs[1], ValueError)
+    assert all(isinstance(errs[r], threading.BrokenBarrierError) for r in (0, 2))
+
+
+def test_loopback_world_requires_the_stream_ordered_allocator():
+    """The native caching allocator's cudaMalloc can wait on a peer rank's kernel
+    (measured deadlock, bootstrap.py): a loopback world refuses it loudly."""
+    from paper_1902_00465_b200.bootstrap import LoopbackWorld
+
+    if torch.cuda.memory.get_allocator_backend() == "cudaMallocAsync":
+        pytest.skip("this process already runs the stream-ordered allocator")
+    with pytest.raises(errors.ConfigurationError, match="cudaMallocAsync"):
+        LoopbackWorld(2)
+    LoopbackWorld(1)  # a single rank never waits on a peer
