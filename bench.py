@@ -2,15 +2,15 @@
 
 One step = one cross-replica all_reduce("premean" = all_sum(g/R))
 of a 64 MiB fp32 gradient fusion buffer per replica, in place in the registered
-pool (zero-copy), by the two-shot NVLink kernel (K2).
+pool (zero-copy): the flat virtual kernel at N=1, the two-shot / NVLS kernels at N>1.
 
   python bench.py                      # N=1: R=8 replicas emulated on one B200
   torchrun --nproc-per-node N bench.py --gpus N   # N ranks, one per GPU, NVLink P2P
   python bench.py --impl reference     # the reference's CPU path (oracle port), host cores
 
-At N=1 the 8 replicas live in one GPU's HBM and the same kernel runs as one
-cooperative launch (replica = blockIdx.y): HBM-bound. At N>1 each GPU is one replica
-and the kernel's loads/stores cross NVLink: NVLink-bound.
+At N=1 the 8 replicas live in one GPU's HBM and one barrier-free launch folds every
+16-byte position of all 8 buffers (ar_virtual_flat): HBM-bound. At N>1 each GPU is
+one replica and the kernel's loads/stores cross NVLink: NVLink-bound.
 
 value = n_gpus x busBW (nccl-tests busBW = 2(R-1)/R * S / t, per GPU), i.e. the
 aggregate bus bandwidth of the job. L2 is flushed (256 MiB write + 256 MiB read) between timed
@@ -59,6 +59,8 @@ def parse():
                         "256 MiB (the flush's write-backs complete before the step; L2 clean and cold)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=10.0)
+    p.add_argument("--ref-budget", type=float, default=150.0,
+                   help="seconds cap on the --impl reference timed steps (whole Graph.evaluate steps)")
     p.add_argument("--e2e-steps", type=int, default=10)
     return p.parse_args()
 
@@ -173,29 +175,46 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (oracle port), all host threads."""
-    from oracle.cpu_baseline import host_cores, time_port
+    """--impl reference: the reference's OWN CPU path -- its Graph.evaluate of the
+    stitched in-process program (oracle/_ref, copied by oracle/ref_vendor.py; numpy
+    runs it on one core) -- for --steps whole steps after --warmup. The oracle port
+    sliced over every host core is reported beside it as a labelled extra."""
+    from oracle.cpu_baseline import host_cores, reference_available, time_port, time_reference
 
     n = args.replicas if world == 1 else world
     count = args.bytes // 4
     if rank != 0:
         return None
     cores = host_cores()
-    # bounded sample: whole stitched steps of the full workload for ~budget seconds
-    sec, steps, thr = time_port(n, count, args.kind, budget_s=args.cpu_budget, threads=cores,
-                                max_steps=max(1, args.steps))
+    if reference_available():
+        sec, steps, thr = time_reference(n, count, args.kind, budget_s=args.ref_budget, max_steps=max(1, args.steps),
+                                         warmup=max(1, args.warmup))
+        kind = "reference"
+        sample = (f"{steps} whole steps of the reference's own Graph.evaluate (oracle/_ref) on the stitched program: "
+                  f"{n} div-by-{n} nodes + {n} nary_sum sites over {n} replicas x {args.bytes >> 20} MiB f32 "
+                  f"(graph.py:514-522); numpy single-threaded: 1 core active of {cores}")
+    else:  # no vendored reference: the validated port (tests/test_oracle.py)
+        sec, steps, thr = time_port(n, count, args.kind, budget_s=args.cpu_budget, threads=cores,
+                                    max_steps=max(1, args.steps))
+        kind = "port"
+        sample = (f"{steps} whole stitched steps ({n} nary_{args.kind} sites x {n} replicas x "
+                  f"{args.bytes >> 20} MiB f32), threads={thr}")
     bw = busbw(args.bytes, n, sec) * world
     line = {
         "metric": "all_reduce bus GB/s (aggregate, 64 MiB fp32 premean)",
-        "value": bw, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": 1,
+        "value": bw, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": max(1, args.warmup),
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "impl": "reference",
         "config": _config(args, world),
-        "cpu_baseline": {"value": bw, "unit": "GB/s", "cores": thr, "kind": "port",
-                         "sample": f"{steps} whole stitched steps ({n} nary_{args.kind} sites x {n} replicas x "
-                                   f"{args.bytes >> 20} MiB f32), threads={thr}"},
+        "cpu_baseline": {"value": bw, "unit": "GB/s", "cores": thr, "kind": kind, "sample": sample},
         "e2e": {"value": bw, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if kind == "reference" and not args.no_cpu_baseline:
+        psec, psteps, pthr = time_port(n, count, args.kind, budget_s=args.cpu_budget, threads=cores, max_steps=50)
+        line["port_all_cores"] = {"value": busbw(args.bytes, n, psec) * world, "unit": "GB/s", "cores": pthr,
+                                  "kind": "port", "steps": psteps,
+                                  "note": "oracle/cpu_baseline.py port of the same folds, message sliced over "
+                                          "every host core (an upper bound on a parallelised reference)"}
     return line
 
 
@@ -232,6 +251,8 @@ def run_ours(args, rank, world, local):
 
         def step():
             comm.all_reduce(bufs, args.kind, outs=bufs, algo=args.algo)
+
+        args.chosen_algo = comm.algorithm_for(bufs[0], args.kind, out=bufs[0], algo=args.algo)
     else:
         n = world
         comm = Communicator(device=local, pool_bytes=pool)
@@ -298,7 +319,8 @@ def run_ours(args, rank, world, local):
     if world == 1:
         alg_bytes = 2.0 * n * args.bytes  # every replica buffer read once, written once
         achieved = alg_bytes / (ms / 1e3) / 1e9
-        kname = f"ar_twoshot<f32,premean,{n}>"
+        kname = {"flat": f"ar_virtual_flat<f32,{args.kind},{n}>", "twoshot": f"ar_twoshot<f32,{args.kind},{n}>",
+                 "oneshot": f"ar_oneshot<f32,{args.kind},{n}>"}.get(args.chosen_algo, args.chosen_algo)
         traffic, tsrc = ncu_traffic(f"{kname}@{args.bytes}")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                     "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
@@ -336,12 +358,17 @@ def run_ours(args, rank, world, local):
         "step_ms_min": min(times), "step_ms_median": statistics.median(times),
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        from oracle.cpu_baseline import time_port
+        from oracle.cpu_baseline import reference_available, time_port, time_reference
 
-        sec, steps, thr = time_port(n, count, args.kind, budget_s=args.cpu_budget, threads=1, max_steps=50)
-        line["cpu_baseline"] = {"value": busbw(args.bytes, n, sec), "unit": "GB/s", "cores": thr, "kind": "port",
-                                "sample": f"{steps} whole stitched steps ({n} nary_{args.kind} sites x {n} replicas "
-                                          f"x {args.bytes >> 20} MiB f32), single-threaded numpy as the reference",
+        if reference_available():
+            sec, steps, thr = time_reference(n, count, args.kind, budget_s=args.cpu_budget, max_steps=50, warmup=1)
+            kind, what = "reference", "steps of the reference's own Graph.evaluate (oracle/_ref) on"
+        else:
+            sec, steps, thr = time_port(n, count, args.kind, budget_s=args.cpu_budget, threads=1, max_steps=50)
+            kind, what = "port", "stitched steps of the oracle port of"
+        line["cpu_baseline"] = {"value": busbw(args.bytes, n, sec), "unit": "GB/s", "cores": thr, "kind": kind,
+                                "sample": f"{steps} whole {what} the stitched program ({n} nary_{args.kind} sites x "
+                                          f"{n} replicas x {args.bytes >> 20} MiB f32), single-threaded numpy",
                                 "ms_per_step": sec * 1e3}
     comm.close()
     return line

@@ -74,6 +74,10 @@ enum {
                           AUTO picks it whenever dst lies in the region */
   RP_ALGO_RELAY = 4,   /* broadcast, multi-process: pipelined tiles root -> owner ->
                           peers over NVLink (P2P stores); AUTO above 1 MiB */
+  RP_ALGO_FLAT = 5,    /* all_reduce, virtual communicator: one barrier-free kernel over
+                          the flat range -- per 16-byte position all R operands loaded,
+                          folded in rank order, stored to all R outputs (every buffer
+                          read and written once). AUTO picks it for virtual replicas */
 };
 
 /* Status codes -> reference exception (errors.py). */

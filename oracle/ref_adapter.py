@@ -1,7 +1,11 @@
-"""Import the reference package (``/root/reference/pkg/src/replicator``) for fixture
-generation. TEST INFRASTRUCTURE ONLY -- runs in the build container; the GPU box has
-no ``/root/reference`` and nothing under ``tests -m gpu``, ``smoke()`` or ``bench.py``
-imports this module.
+"""Import the reference package (``replicator``) -- TEST INFRASTRUCTURE ONLY.
+
+Source: ``oracle/_ref/replicator``, the git-ignored copy ``oracle/ref_vendor.py``
+makes from ``/root/reference/pkg/src/replicator`` at build time (it travels to the
+GPU box; ``/root/reference`` does not), else ``/root/reference/pkg/src`` itself.
+Used to generate the golden fixtures, by the GPU tests that run the reference's own
+``Graph.evaluate`` through this repo's communicators (the checker, never the thing
+measured), and by ``bench.py --impl reference`` (the reference's own CPU path).
 
 Applies the survey's 6-line 0-d shim: ``Tensor.__init__``
 promotes rank-0 arrays to shape (1,) via ``np.ascontiguousarray``
@@ -16,7 +20,9 @@ import sys
 
 import numpy as np
 
-REF_SRC = os.environ.get("RP_REFERENCE_SRC", "/root/reference/pkg/src")
+_VENDORED = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref")
+REF_SRC = os.environ.get("RP_REFERENCE_SRC") or (
+    _VENDORED if os.path.isdir(os.path.join(_VENDORED, "replicator")) else "/root/reference/pkg/src")
 
 
 def available() -> bool:

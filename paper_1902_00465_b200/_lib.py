@@ -25,10 +25,11 @@ AUTO, ONESHOT, TWOSHOT = 0, 1, 2
 DIRECT, SCATTER = 1, 2
 NVLS = 3
 RELAY = 4
+FLAT = 5
 # fused optimizer apply (rp_all_reduce_apply)
 OPT_SGD, OPT_ADAM, OPT_ADAMW = 0, 1, 2
 ALGOS = {"auto": AUTO, "oneshot": ONESHOT, "twoshot": TWOSHOT, "direct": DIRECT, "scatter": SCATTER, "nvls": NVLS,
-         "relay": RELAY}
+         "relay": RELAY, "flat": FLAT}
 # link kinds (rp_comm_import topology discovery, rp_topology_check)
 LINK_SELF, LINK_NVLINK, LINK_PCIE, LINK_NONE, LINK_UNKNOWN, LINK_SAME_DEVICE, LINK_LOOPBACK = range(7)
 # layouts

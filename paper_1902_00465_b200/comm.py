@@ -167,6 +167,21 @@ class _Base:
         cap). Set identically on every rank (include/rp.h rp_comm_set_block_cap)."""
         _lib.check(self._lib.rp_comm_set_block_cap(self._handle, int(blocks)), "set_block_cap")
 
+    def algorithm_for(self, x: torch.Tensor, kind: str = "sum", out: torch.Tensor | None = None,
+                      comm_dtype: torch.dtype | None = None, algo: str = "auto") -> str:
+        """The kernel family all_reduce_tensor(x, kind, out, comm_dtype, algo) runs:
+        "oneshot", "twoshot", "nvls" or (virtual replicas) "flat" (include/rp.h
+        rp_all_reduce_algo). ``x``/``out``: this rank's tensors (a virtual
+        communicator: replica 0's)."""
+        out = x if out is None else out
+        code = dtype_code(x.dtype)
+        ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
+        chosen = ctypes.c_int(0)
+        _lib.check(self._lib.rp_all_reduce_algo(self._handle, x.data_ptr(), out.data_ptr(), x.numel(), code, ccode,
+                                                dtype_code(out.dtype), _op(kind), _algo(algo), ctypes.byref(chosen)),
+                   "all_reduce_algo")
+        return {1: "oneshot", 2: "twoshot", 3: "nvls", 5: "flat"}[chosen.value]
+
     # -- host buffers in, host buffer out ------------------------------------
     HOST_CHUNK_BYTES = 8 << 20
     HOST_RING = 3
@@ -398,19 +413,6 @@ class Communicator(_Base):
         if od is not out:
             out.copy_(od)
         return out
-
-    def algorithm_for(self, x: torch.Tensor, kind: str = "sum", out: torch.Tensor | None = None,
-                      comm_dtype: torch.dtype | None = None, algo: str = "auto") -> str:
-        """The kernel family all_reduce_tensor(x, kind, out, comm_dtype, algo) runs:
-        "oneshot", "twoshot" or "nvls" (include/rp.h rp_all_reduce_algo)."""
-        out = x if out is None else out
-        code = dtype_code(x.dtype)
-        ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
-        chosen = ctypes.c_int(0)
-        _lib.check(self._lib.rp_all_reduce_algo(self._handle, x.data_ptr(), out.data_ptr(), x.numel(), code, ccode,
-                                                dtype_code(out.dtype), _op(kind), _algo(algo), ctypes.byref(chosen)),
-                   "all_reduce_algo")
-        return {1: "oneshot", 2: "twoshot", 3: "nvls"}[chosen.value]
 
     def all_gather_ragged(self, x: torch.Tensor) -> list[torch.Tensor]:
         """shapes may differ across ranks in the leading dimension

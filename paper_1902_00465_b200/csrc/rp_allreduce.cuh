@@ -175,6 +175,13 @@ __device__ __forceinline__ uint32_t claim_tile(const CollArgs& a, int rank, int 
   return __shfl_sync(0xffffffffu, t, 0);
 }
 
+// The same per-warp claim on an explicit counter.
+__device__ __forceinline__ uint32_t claim_ctr(uint32_t* ctr) {
+  uint32_t t = 0;
+  if ((threadIdx.x & 31) == 0) t = atomicAdd(ctr, 1u);
+  return __shfl_sync(0xffffffffu, t, 0);
+}
+
 // Per-call phase-barrier bases, read by every block at kernel start: rank p's
 // counter on phase row k must reach seen[k] + 1 (one arrival per rank per call).
 struct PhaseBase {
@@ -453,6 +460,72 @@ __global__ void __launch_bounds__(kThreads) ar_oneshot(const CollArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K2v: flat all-reduce for VIRTUAL replicas (all NR replicas' buffers in this
+// GPU's HBM). Nothing crosses a link, so nothing needs partitioning by rank:
+// every warp claims tiles of the flat vector range from one counter and, per
+// 16-byte position, loads all NR operands, folds them in rank order and stores
+// the result into all NR outputs -- each buffer read once and written once (the
+// HBM minimum, 2*NR*S), with no barrier at all. The two-shot's rank chunks, two
+// phase barriers and one-rank-per-blockIdx.y grid (144 of 148 SMs at NR=8) were
+// pure overhead here. In place is safe: a position's NR loads precede its NR
+// stores in the same thread. The last block to finish zeroes the counters.
+// ---------------------------------------------------------------------------
+#ifndef RP_VFLAT_U
+#define RP_VFLAT_U(NR) ((NR) > 4 ? 2 : 4)
+#endif
+template <int DT, int OP, int NR>
+__global__ void __launch_bounds__(kThreads, 1) ar_virtual_flat(const CollArgs a) {
+  using T = typename DType<DT>::T;
+  using A = typename DType<DT>::Acc;
+  if (rp_aborted(a.t, 0)) return;
+  const size_t V = (a.count + (16 / sizeof(T)) - 1) / (16 / sizeof(T));
+  const uint32_t tv = a.tile_v;
+  const uint32_t ntiles = (uint32_t)((V + tv - 1) / tv);
+  uint32_t* ctr = a.t.sig[0] + RP_ST_VFLAT_CTR;
+  const int lane = threadIdx.x & 31;
+  bool ali = true, alo = true;
+#pragma unroll
+  for (int p = 0; p < NR; ++p) {
+    ali = ali && aligned16(a.src[p]);
+    alo = alo && aligned16(a.dst[p]);
+  }
+  constexpr int U = RP_VFLAT_U(NR);
+  for (uint32_t t = claim_ctr(ctr); t < ntiles; t = claim_ctr(ctr)) {
+    const size_t lo = (size_t)t * tv;
+    const size_t hi = std::min(lo + tv, V);
+    for (size_t base = lo + lane; base < hi; base += 32 * U) {
+      uint4 x[U][NR];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = base + (size_t)u * 32;
+        if (v < hi) {
+#pragma unroll
+          for (int p = 0; p < NR; ++p) x[u][p] = load_src<T>(a, a.src[p], v, ali);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = base + (size_t)u * 32;
+        if (v < hi) {
+          const uint4 r = fold_packet<T, A, OP, NR>(x[u]);
+#pragma unroll
+          for (int p = 0; p < NR; ++p) store_dst<T>(a, a.dst[p], v, alo, r);
+        }
+      }
+    }
+  }
+  // last block out resets the counters for the next call (all claims are done)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.t.sig[0] + RP_ST_VFLAT_DONE, 1u) == gridDim.x - 1) {
+      state_store(a.t, 0, RP_ST_VFLAT_CTR, 0u);
+      state_store(a.t, 0, RP_ST_VFLAT_DONE, 0u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // world == 1: local op (identity fold) with the same conversion rules
 // ---------------------------------------------------------------------------
 template <int DT, int OP>
@@ -493,6 +566,18 @@ const void* pick_ar(int algo, int world, int push) {
                                      : (const void*)ar_twoshot_dyn<DT, OP, NR, true>;           \
     return algo == RP_ALGO_ONESHOT ? (const void*)ar_oneshot<DT, OP, NR>                        \
                                    : (const void*)ar_twoshot_dyn<DT, OP, NR, false>;
+  if (algo == RP_ALGO_FLAT) {
+    switch (world) {
+      case 2: return (const void*)ar_virtual_flat<DT, OP, 2>;
+      case 3: return (const void*)ar_virtual_flat<DT, OP, 3>;
+      case 4: return (const void*)ar_virtual_flat<DT, OP, 4>;
+      case 5: return (const void*)ar_virtual_flat<DT, OP, 5>;
+      case 6: return (const void*)ar_virtual_flat<DT, OP, 6>;
+      case 7: return (const void*)ar_virtual_flat<DT, OP, 7>;
+      case 8: return (const void*)ar_virtual_flat<DT, OP, 8>;
+      default: return nullptr;
+    }
+  }
   switch (world) {
     case 1: return (const void*)ar_single<DT, OP>;
     RP_CASE(2) RP_CASE(3) RP_CASE(4) RP_CASE(5) RP_CASE(6) RP_CASE(7) RP_CASE(8)

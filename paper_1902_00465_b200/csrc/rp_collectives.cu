@@ -273,7 +273,7 @@ void fill_ptrs(rp_comm* c, CollArgs& a, const void* const* src, void* const* dst
 // the per-block %globaltimer stamps (rp_device.cuh rp_trace) and append them as
 // one JSON line per launch. Tracing synchronises the stream.
 int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t stream, const char* tag,
-                int threads = kThreads) {
+                int threads = kThreads, bool coop = true) {
   const char* path = getenv("RP_TRACE");
   const size_t n = (size_t)grid.x * grid.y * 8;
   unsigned long long* buf = nullptr;
@@ -284,7 +284,7 @@ int launch_coll(rp_comm* c, const void* fn, dim3 grid, CollArgs& a, cudaStream_t
     a.trace = buf;
   }
   void* args[] = {&a};
-  const int rc = rp_launch(c, fn, grid, dim3(threads), args, 0, stream);
+  const int rc = rp_launch(c, fn, grid, dim3(threads), args, 0, stream, coop);
   if (path) {
     std::vector<unsigned long long> h(n);
     cudaStreamSynchronize(stream);
@@ -352,6 +352,13 @@ int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* ds
                        int dtype_comm, int dtype_out, int op, int algo) {
   if (algo != RP_ALGO_AUTO) return algo;
   const int W = c->world;
+  // virtual replicas share one GPU's HBM: the flat kernel reads and writes every
+  // buffer once with no barrier (RP_VIRTUAL_ALGO=rank restores the rank-partitioned
+  // one-shot / two-shot below, for A/B)
+  if (c->is_virtual && W > 1) {
+    const char* va = getenv("RP_VIRTUAL_ALGO");
+    if (!(va && va[0] == 'r')) return RP_ALGO_FLAT;
+  }
   const size_t bytes = count * rp_dtype_size(dtype_comm);
   // NVLS (in-switch reduce + multicast store) moves (N+1)/N of the message per
   // link direction against 2(N-1)/N for the two-shot: it wins from N=4 on, above
@@ -422,6 +429,22 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
     if (src[0] != dst[0] || dtype_in != dtype_comm || dtype_out != dtype_comm)
       return rp_fail(RP_ERR_INVALID, "all_reduce(nvls): in place, without a cast");
     return rp_nvls_launch(c, dst[0], count, dtype_comm, op, stream, dyn_launch, a);
+  }
+  if (algo == RP_ALGO_FLAT) {
+    if (!c->is_virtual) return rp_fail(RP_ERR_INVALID, "all_reduce(flat): needs a virtual communicator");
+    const void* fn = pick_ar_any(dtype_comm, op, RP_ALGO_FLAT, W, 0);
+    if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce(flat): unsupported replica count (2..8)");
+    // one co-resident wave on EVERY SM; tiles of 256..4096 vectors, >= 4 per warp
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+    int blocks = (int)std::min<size_t>((size_t)occ * c->num_sms, (V + 31) / 32);
+    if (c->cap() > 0) blocks = std::min(blocks, c->cap());
+    blocks = std::max(blocks, 1);
+    const size_t warps = (size_t)blocks * (kThreads / 32);
+    size_t tv = V / (warps * 4);
+    if (const char* e = getenv("RP_VFLAT_TILE")) tv = (size_t)atoi(e);
+    a.tile_v = (uint32_t)std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
+    return launch_coll(c, fn, dim3(blocks), a, stream, "virtual_flat", kThreads, /*coop=*/false);
   }
   if (algo != RP_ALGO_ONESHOT && algo != RP_ALGO_TWOSHOT)
     return rp_fail(RP_ERR_INVALID, "all_reduce: unknown algorithm");

@@ -71,9 +71,9 @@ int64_t rp_wave_per_rank(rp_comm* c, int per_sm) {
 }
 
 int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, size_t smem,
-              cudaStream_t stream) {
+              cudaStream_t stream, bool coop) {
   cudaError_t e;
-  if (c->is_virtual && c->world > 1)
+  if (coop && c->is_virtual && c->world > 1)
     e = cudaLaunchCooperativeKernel(func, grid, block, args, smem, stream);
   else
     e = cudaLaunchKernel(func, grid, block, args, smem, stream);

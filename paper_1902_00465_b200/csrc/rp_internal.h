@@ -43,6 +43,10 @@
 // the count already consumed by earlier calls)
 #define RP_ST_BN_GRID_CTR (RP_ST_PH_SEEN + 8)
 #define RP_ST_BN_GRID_BASE (RP_ST_PH_SEEN + 9)
+// flat virtual all-reduce (ar_virtual_flat): tile-claim counter and blocks-done
+// counter, zeroed by the call's last block (so a launch carries no host state)
+#define RP_ST_VFLAT_CTR (RP_ST_PH_SEEN + 10)
+#define RP_ST_VFLAT_DONE (RP_ST_PH_SEEN + 11)
 #define RP_SIGNAL_BYTES (64 * 1024)  // signal region ahead of the data
 #define RP_ALIGN 256
 // Pool layout (every rank identical):
@@ -188,7 +192,7 @@ int rp_launch_bn_bwd_stats(rp_comm* c, const void* x, const void* dy, int dtype,
 // blocks must be co-resident because they wait on one another), plain launch
 // otherwise (one rank per process; blocks only wait on peers' blocks).
 int rp_launch(rp_comm* c, const void* func, dim3 grid, dim3 block, void** args, size_t smem,
-              cudaStream_t stream);
+              cudaStream_t stream, bool coop = true);
 // Blocks per rank for a collective kernel given its per-block occupancy.
 int rp_blocks_per_rank(rp_comm* c, const void* func, int threads, int want);
 // Co-resident block budget per rank for kernels that size their own grid (BN):

@@ -252,6 +252,63 @@ def body_mesh_seam(rank, world, env):
     comm.close()
 
 
+def _stitched_reference(G, T, xs, dtype):
+    """The reference's own in-process evaluation of one replica site per collective
+    kind over all replicas' inputs (the stitched folds, graph.py:506-540)."""
+    shape = np.shape(xs[0])
+    g = G.Graph()
+    ins = [g.add_node("input", [], {"shape": shape, "dtype": dtype}) for _ in xs]
+    sites = {"sum": g.add_node("nary_sum", ins), "mean": g.add_node("nary_mean", ins),
+             "max": g.add_node("nary_max", ins),
+             "gather": g.add_node("pack", ins) if shape == () else g.add_node("concat", ins, {"axis": 0}),
+             "broadcast": g.add_node("pick0", ins)}
+    g.finalize()
+    res = g.evaluate(list(sites.values()), {i: T.Tensor(x, dtype=dtype) for i, x in zip(ins, xs)})
+    return {k: r.np for k, r in zip(sites, res)}
+
+
+def body_reference_graph(rank, world, env):
+    """the REFERENCE's own engine with this repo as its
+    communicator. Each rank builds the reference Graph with one ``mesh_collective``
+    per kind (sum / mean / max / gather / broadcast) and evaluates it with
+    ``runtime={"communicator": Communicator}`` (graph.py:565-583, :706-707); every
+    result must equal, bit for bit, the reference's own stitched in-process fold of
+    all ranks' inputs (nary_* / concat / pack / pick0, graph.py:506-540), for
+    scalars (the seam's (1,) promotion included), 2x3 and 1000-element f32 / f64."""
+    from oracle import ref_adapter
+    from paper_1902_00465_b200.comm import Communicator
+
+    if not ref_adapter.available():
+        pytest.skip("reference package not vendored (oracle/ref_vendor.py)")
+    T, G, _, _ = ref_adapter.load()
+    comm = Communicator(device=env.device, bootstrap=env.bootstrap, pool_bytes=16 << 20)
+    kinds = ("sum", "mean", "max", "gather", "broadcast")
+    for dtype, npd in (("f32", np.float32), ("f64", np.float64)):
+        for shape in ((), (2, 3), (1000,)):
+            xs = [np.random.default_rng(500 + 7 * r + len(shape)).standard_normal(shape).astype(npd)
+                  for r in range(world)]
+            g = G.Graph()
+            x = g.add_node("input", [], {"shape": shape, "dtype": dtype})
+            nodes = [g.add_node("mesh_collective", [x], {"ckind": k, "label": f"{k}/{dtype}/{shape}",
+                                                          "num_replicas": world}) for k in kinds]
+            g.finalize()
+            res = g.evaluate(nodes, {x: T.Tensor(xs[rank], dtype=dtype)}, runtime={"communicator": comm})
+            want = _stitched_reference(G, T, xs, dtype)
+            for k, r in zip(kinds, res):
+                assert isinstance(r, T.Tensor) and r.dtype == dtype, (k, type(r), r.dtype)
+                assert r.np.reshape(-1).tobytes() == want[k].reshape(-1).tobytes(), (k, dtype, shape)
+    # no communicator at runtime: the reference's own EvaluationError (graph.py:567-569)
+    g = G.Graph()
+    x = g.add_node("input", [], {"shape": (2,), "dtype": "f64"})
+    y = g.add_node("mesh_collective", [x], {"ckind": "sum", "label": "none", "num_replicas": world})
+    g.finalize()
+    from replicator import errors as ref_errors
+    with pytest.raises(ref_errors.EvaluationError):
+        g.evaluate([y], {x: T.Tensor(np.ones(2))})
+    comm.check()
+    comm.close()
+
+
 def body_bn(rank, world, env):
     from oracle import collectives as O
     from paper_1902_00465_b200.replicator import CrossReplicaBatchNorm, Replicator

@@ -103,6 +103,15 @@ def test_gather_broadcast_loopback(world):
 
 
 @pytest.mark.timeout(300)
+@W24
+def test_reference_graph_evaluate_through_communicator_loopback(world):
+    from oracle import ref_adapter
+    if not ref_adapter.available():
+        pytest.skip("reference package not vendored (oracle/ref_vendor.py)")
+    run_loopback("body_reference_graph", world)
+
+
+@pytest.mark.timeout(300)
 def test_reference_mesh_seam_replay_loopback():
     run_loopback("body_mesh_seam", 2)
 

@@ -77,6 +77,10 @@ def test_reference_mesh_seam_replay():
     run_world("body_mesh_seam", world=2)
 
 
+def test_reference_graph_evaluate_through_communicator_multiprocess():
+    run_world("body_reference_graph")
+
+
 def test_cross_replica_bn_autograd_multiprocess():
     run_world("body_bn")
 

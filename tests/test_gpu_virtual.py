@@ -56,7 +56,7 @@ def impl(request, monkeypatch):
 
 # --- all_reduce vs the reference's stitched folds ---------------------------
 
-@pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot", "flat"])
 @pytest.mark.parametrize("kind", ["sum", "mean", "max", "premean"])
 def test_all_reduce_matches_reference_folds(folds, algo, kind, impl):
     for key, dtype, n, shape in fold_cases(folds):
@@ -91,7 +91,7 @@ def test_all_reduce_sizes_f32(n, count, impl):
     xs_np = [rng.standard_normal(count).astype(np.float32) for _ in range(n)]
     for kind in ("sum", "premean", "max"):
         want = O.FOLDS[kind](xs_np)
-        for algo in ("oneshot", "twoshot"):
+        for algo in ("oneshot", "twoshot", "flat"):
             outs = vcomm(n).all_reduce([to_dev(x) for x in xs_np], kind, algo=algo)
             for o in outs:
                 assert host(o).tobytes() == want.tobytes(), (kind, algo)
@@ -105,7 +105,7 @@ def test_all_reduce_misaligned_views(impl):
     want = O.fold_sum([host(x) for x in xs])
     outs_base = [torch.zeros(10003, device=DEV) for _ in range(n)]
     outs = [o[3:10003] for o in outs_base]
-    for algo in ("oneshot", "twoshot"):
+    for algo in ("oneshot", "twoshot", "flat"):
         vcomm(n).all_reduce(xs, "sum", outs=outs, algo=algo)
         for o in outs:
             assert host(o).tobytes() == want.tobytes()
@@ -119,10 +119,19 @@ def test_all_reduce_large_f32_premean_8_replicas(impl):
     gens = [torch.Generator(device=DEV).manual_seed(1234 + r) for r in range(n)]
     xs = [torch.randn(count, device=DEV, generator=g) for g in gens]
     comm = vcomm(n, pool=256 << 20)
-    outs = comm.all_reduce(xs, "premean")
     want = O.fold_premean([host(x) for x in xs])
-    for o in outs:
-        assert host(o).tobytes() == want.tobytes()
+    for algo in ("auto", "twoshot"):
+        outs = comm.all_reduce(xs, "premean", algo=algo)
+        for o in outs:
+            assert host(o).tobytes() == want.tobytes(), algo
+    # the bench's form: in place in the pool, the flat kernel AUTO picks
+    assert comm.algorithm_for(xs[0], "premean") == "flat"
+    bufs = comm.alloc(count, torch.float32)
+    for b, x in zip(bufs, xs):
+        b.copy_(x)
+    comm.all_reduce(bufs, "premean", outs=bufs)
+    for b in bufs:
+        assert host(b).tobytes() == want.tobytes()
 
 
 def test_staged_in_pieces_when_pool_small(impl):
@@ -130,7 +139,7 @@ def test_staged_in_pieces_when_pool_small(impl):
     comm = VirtualCommunicator(n, device=0, pool_bytes=16 << 20)
     rng = np.random.default_rng(11)
     xs_np = [rng.standard_normal(count).astype(np.float32) for _ in range(n)]
-    for algo in ("oneshot", "twoshot"):
+    for algo in ("oneshot", "twoshot", "flat"):
         outs = comm.all_reduce([to_dev(x) for x in xs_np], "sum", algo=algo)
         want = O.fold_sum(xs_np)
         for o in outs:
