@@ -457,26 +457,31 @@ class Replicator:
     def all_sum(self, x: torch.Tensor, label: str | None = None) -> torch.Tensor:
         return self.all_reduce(x, "sum", label)
 
-    def all_gather(self, x: torch.Tensor, label: str | None = None, ragged: bool = False):
-        """Returns (R,) + x.shape: every replica's x in replica order. ``ragged=True``
-        (leading dimensions may differ across replicas) returns the list
-        [x_0, ..., x_{R-1}] instead."""
+    def all_gather(self, x: torch.Tensor, label: str | None = None, ragged: bool = False, stack: bool = False):
+        """every replica gets the list [x_0, ..., x_{R-1}] in replica
+        order (views of one gathered buffer). ``ragged=True``: leading dimensions may
+        differ across replicas. ``stack=True``: the one (R,) + x.shape
+        tensor instead of the list (same bits, no split)."""
+        if ragged and stack:
+            raise errors.ShapeError("all_gather: a ragged gather cannot be stacked")
         if self.is_virtual:
             if self.comm.world == 1:
-                return [x.clone()] if ragged else x.unsqueeze(0).clone()
-            if ragged:
+                g = x.unsqueeze(0).clone()
+            elif ragged:
                 parts = self._collective(("all_gather_ragged", label, tuple(x.shape[1:]), x.dtype), x.detach(),
                                          lambda xs: self.comm.all_gather_ragged(xs))
                 return [_novjp(x, t, "all_gather") for t in parts]
-            y = self._collective(("all_gather", label, tuple(x.shape), x.dtype), x.detach(),
-                                 lambda xs: self.comm.all_gather(xs))
-            return _novjp(x, y, "all_gather")
-        self._verify(label, "gather", x.shape[1:] if ragged else x.shape, x.dtype)
-        if ragged:
-            if torch.is_grad_enabled() and x.requires_grad:
-                raise errors.NotDifferentiableError("ragged all_gather has no VJP; gather x.detach()")
-            return self.comm.all_gather_ragged(x)
-        return _AllGatherFn.apply(x, self.comm)
+            else:
+                g = _novjp(x, self._collective(("all_gather", label, tuple(x.shape), x.dtype), x.detach(),
+                                               lambda xs: self.comm.all_gather(xs)), "all_gather")
+        else:
+            self._verify(label, "gather", x.shape[1:] if ragged else x.shape, x.dtype)
+            if ragged:
+                if torch.is_grad_enabled() and x.requires_grad:
+                    raise errors.NotDifferentiableError("ragged all_gather has no VJP; gather x.detach()")
+                return self.comm.all_gather_ragged(x)
+            g = _AllGatherFn.apply(x, self.comm)
+        return g if stack else list(g.unbind(0))
 
     def broadcast(self, x: torch.Tensor, root: int = 0, label: str | None = None) -> torch.Tensor:
         if self.is_virtual:

@@ -407,7 +407,7 @@ def body_autograd(rank, world, env):
         np.testing.assert_allclose(H(x.grad).numpy(), wsum * scale, rtol=1e-12, atol=1e-12)
     Ws = [np.random.default_rng(320 + q).standard_normal((world, n)) for q in range(world)]
     x = torch.from_numpy(x0).to(dev).requires_grad_(True)
-    g = repl.all_gather(x)
+    g = repl.all_gather(x, stack=True)
     assert g.shape == (world, n)
     (g * torch.from_numpy(Ws[rank]).to(dev)).sum().backward()
     np.testing.assert_allclose(H(x.grad).numpy(), sum(W[rank] for W in Ws), rtol=1e-12, atol=1e-12)

@@ -473,8 +473,13 @@ def test_replicator_run_all_sum_and_protocol_error():
     with pytest.raises(errors.ProtocolError):
         repl.run(lambda x: repl.all_sum(x, label=f"g{repl.replica_id}"),
                  lambda r: torch.ones(2, device=DEV))
-    gathered = repl.run(lambda x: repl.all_gather(x), lambda r: torch.full((2,), float(r), device=DEV))
+    gathered = repl.run(lambda x: repl.all_gather(x, stack=True), lambda r: torch.full((2,), float(r), device=DEV))
     assert host(gathered[1]).tolist() == [[0, 0], [1, 1], [2, 2]]
+    # the default is the rank-ordered list [t_0, ..., t_{N-1}]
+    lists = repl.run(lambda x: repl.all_gather(x), lambda r: torch.full((2,), float(r), device=DEV))
+    assert all(isinstance(l, list) and [host(t).tolist() for t in l] == [[0, 0], [1, 1], [2, 2]] for l in lists)
+    scal = repl.run(lambda x: repl.all_gather(x), lambda r: torch.tensor(float(7 + r), device=DEV))
+    assert [float(host(t)) for t in scal[0]] == [7.0, 8.0, 9.0]  # SPEC's N=3 scalars example
     repl.comm.close()
 
 

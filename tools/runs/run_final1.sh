@@ -8,5 +8,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python tools/launch_shares.py gpurun_out/f1_launches.csv "# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialised): $CMD" > gpurun_out/f1_launches.txt; cat gpurun_out/f1_launches.txt | head -8
 ncu --set full --clock-control none --import-source on -k regex:ar_twoshot_dyn -s 3 -c 1 -o gpurun_out/f1_ar $CMD > /dev/null 2>&1
 ncu -i gpurun_out/f1_ar.ncu-rep --page raw --csv > gpurun_out/f1_ar_raw.csv 2>/dev/null; python tools/ncu_summary.py gpurun_out/f1_ar_raw.csv
-bash tools/run_ncu_bn2.sh
+bash tools/runs/run_ncu_bn2.sh
 rm -f gpurun_out/*.ncu-rep

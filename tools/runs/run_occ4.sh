@@ -8,4 +8,4 @@ for n in 2 4; do
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2951$n bench.py --gpus $n --steps 100 --warmup 10 > gpurun_out/oc_n$n.json 2> gpurun_out/oc_n$n.err; s gpurun_out/oc_n$n.json
 done
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29519 bench.py --gpus 4 --steps 100 --warmup 10 --nvls off > gpurun_out/oc_n4p.json 2> gpurun_out/oc_n4p.err; s gpurun_out/oc_n4p.json
-CUDA_VISIBLE_DEVICES=0 bash tools/run_ncu_bn2.sh
+CUDA_VISIBLE_DEVICES=0 bash tools/runs/run_ncu_bn2.sh

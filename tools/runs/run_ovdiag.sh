@@ -8,4 +8,4 @@ rn 2 --overlap --overlap-dry
 rn 2 --overlap --overlap-priority 0
 rn 2 --overlap --overlap-blocks 8
 rn 2 --overlap --overlap-blocks 8 --overlap-priority 0
-CUDA_VISIBLE_DEVICES=0 bash tools/run_bn_small.sh
+CUDA_VISIBLE_DEVICES=0 bash tools/runs/run_bn_small.sh

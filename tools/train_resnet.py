@@ -165,7 +165,7 @@ def main():
         ms, ar_ms = t.tolist()
     # replicas must stay bit-identical (SPEC.md:399 replica consistency)
     flat = torch.cat([q.detach().reshape(-1) for q in net.parameters()])
-    gathered = repl.all_gather(flat) if world > 1 else flat.unsqueeze(0)
+    gathered = repl.all_gather(flat, stack=True) if world > 1 else flat.unsqueeze(0)
     consistent = bool(all(torch.equal(gathered[r], gathered[0]) for r in range(world)))
     if rank == 0:
         if a.fused:

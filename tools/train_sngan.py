@@ -1,13 +1,16 @@
 """SN-GAN 128x128 class-conditional training step with cross-replica BatchNorm
 (BASELINE.json configs[3]).
 
-Generator: z(120) + class embedding -> 4x4x1024 -> five up-sampling ResNet-free
-blocks (nearest x2, conv3x3, CrossReplicaBatchNorm, ReLU) with channels
-1024, 1024, 512, 256, 128, 64 at 8..128 px -> conv3x3 -> tanh. Every BN in the
-generator is the per-channel cross-replica BN of this repo (K5 forward statistics,
-K5b backward statistics over NVLink). Discriminator: spectrally normalised conv
-stack with a projection head (hinge loss). Both optimizers (Adam, PAPER.md:296's
-SN-GAN hyper-parameters) are wrapped. Synthetic data; global batch = 64 x N
+Generator (SAGAN/BigGAN-style, the survey's 11 cross-replica BN layers, SURVEY.md
+§8a): z(120) + class embedding -> 4x4x1024 -> five up-sampling residual blocks
+1024->1024->512->256->128->64 at 8..128 px, each BN(cin) -> ReLU -> nearest x2 ->
+conv3x3 -> BN(cout) -> ReLU -> conv3x3 plus an up-sampled 1x1 shortcut, then
+BN(64) -> ReLU -> conv3x3 -> tanh: BN widths 1024, 1024, 1024, 512, 512, 256, 256,
+128, 128, 64, 64. Every BN in the generator is the per-channel cross-replica BN of
+this repo (K5 forward statistics, K5b backward statistics over NVLink).
+Discriminator: spectrally normalised conv stack with a projection head (hinge
+loss). Both optimizers (Adam, PAPER.md:296's SN-GAN hyper-parameters) are wrapped.
+Synthetic data; global batch = 64 x N
 (PAPER.md:285). The builder's channel plan follows SURVEY.md §8a.
 
   torchrun --nproc-per-node N tools/train_sngan.py
@@ -29,26 +32,37 @@ SN = nn.utils.spectral_norm
 CH = [1024, 1024, 512, 256, 128, 64]  # 4 -> 128 px
 
 
+class GBlock(nn.Module):
+    """Residual up-sampling block with two cross-replica BNs (BN(cin), BN(cout))."""
+
+    def __init__(self, cin, cout, repl, bn_cls):
+        super().__init__()
+        self.bn1, self.bn2 = bn_cls(cin, repl), bn_cls(cout, repl)
+        self.conv1 = nn.Conv2d(cin, cout, 3, padding=1)
+        self.conv2 = nn.Conv2d(cout, cout, 3, padding=1)
+        self.skip = nn.Conv2d(cin, cout, 1)
+
+    def forward(self, x):
+        h = F.interpolate(F.relu(self.bn1(x)), scale_factor=2, mode="nearest")
+        h = self.conv2(F.relu(self.bn2(self.conv1(h))))
+        return h + self.skip(F.interpolate(x, scale_factor=2, mode="nearest"))
+
+
 class Generator(nn.Module):
     def __init__(self, repl, nz=120, ncls=1000, bn_cls=None):
         super().__init__()
         self.embed = nn.Embedding(ncls, nz)
         self.fc = nn.Linear(2 * nz, 4 * 4 * CH[0])
-        blocks = []
-        for cin, cout in zip(CH[:-1], CH[1:]):
-            blocks += [nn.Conv2d(cin, cout, 3, padding=1), bn_cls(cout, repl)]
-        self.convs = nn.ModuleList(blocks[0::2])
-        self.bns = nn.ModuleList(blocks[1::2])
-        self.bn0 = bn_cls(CH[0], repl)
+        self.blocks = nn.ModuleList([GBlock(a, b, repl, bn_cls) for a, b in zip(CH[:-1], CH[1:])])
+        self.bn_out = bn_cls(CH[-1], repl)
         self.out = nn.Conv2d(CH[-1], 3, 3, padding=1)
 
     def forward(self, z, y):
         h = self.fc(torch.cat([z, self.embed(y)], 1)).view(-1, CH[0], 4, 4)
-        h = F.relu(self.bn0(h.contiguous(memory_format=torch.channels_last)))
-        for conv, bn in zip(self.convs, self.bns):
-            h = F.interpolate(h, scale_factor=2, mode="nearest")
-            h = F.relu(bn(conv(h)))
-        return torch.tanh(self.out(h))
+        h = h.contiguous(memory_format=torch.channels_last)
+        for blk in self.blocks:
+            h = blk(h)
+        return torch.tanh(self.out(F.relu(self.bn_out(h))))
 
 
 class Discriminator(nn.Module):
@@ -131,14 +145,14 @@ def main():
         ms = t.item()
     # the cross-replica BN statistics must be identical on every replica
     rm = torch.cat([b.running_mean for b in G.local.bns])
-    gathered = repl.all_gather(rm) if world > 1 else rm.unsqueeze(0)
+    gathered = repl.all_gather(rm, stack=True) if world > 1 else rm.unsqueeze(0)
     same = bool(all(torch.equal(gathered[r], gathered[0]) for r in range(world)))
     if rank == 0:
         print(json.dumps({"metric": "SN-GAN step (D+G) img/s", "value": world * a.batch / (ms / 1e3), "unit": "img/s",
                           "n_gpus": world, "per_gpu_batch": a.batch, "ms_per_step": ms,
                           "d_loss": float(dl.item()), "g_loss": float(gl.item()),
                           "bn_running_stats_identical": same,
-                          "config": {"resolution": 128, "generator_bn": "CrossReplicaBatchNorm x6 (K5/K5b)",
+                          "config": {"resolution": 128, "generator_bn": "CrossReplicaBatchNorm x11 (K5/K5b; widths 1024x3, 512x2, 256x2, 128x2, 64x2)",
                                      "precision": "bf16 autocast", "data": "synthetic"}}), flush=True)
     repl.comm.close()
     if world > 1:
