@@ -232,9 +232,20 @@ RP_API int rp_all_reduce_apply_v(rp_comm_t comm, const void* const* grad, void* 
                                  float* const* state1, int32_t* const* step, void* stream);
 
 /* The algorithm rp_all_reduce would run for these arguments (RP_ALGO_ONESHOT,
- * RP_ALGO_TWOSHOT or RP_ALGO_NVLS) in *chosen; nothing is launched. */
+ * RP_ALGO_TWOSHOT, RP_ALGO_NVLS or, virtual, RP_ALGO_FLAT) in *chosen; nothing is
+ * launched. */
 RP_API int rp_all_reduce_algo(rp_comm_t comm, const void* src, const void* dst, size_t count, int dtype_in,
                               int dtype_comm, int dtype_out, int op, int algo, int* chosen);
+
+/* The plan rp_all_reduce would follow, for cross-rank agreement checks
+ * (Replicator(check_protocol=True) digests it): plan[0] = algorithm (AUTO
+ * resolved), plan[1] = 1 for the push data-movement form, plan[2] / plan[3] = pool
+ * offset of src / dst, or -1 when outside the pool. Ranks MUST agree on all four
+ * (symmetric placement): a rank passing a pool view where a peer passes a plain
+ * tensor would launch a different kernel against the shared barrier state.
+ * Multi-process communicators only look at this rank's pointers. */
+RP_API int rp_all_reduce_plan(rp_comm_t comm, const void* src, const void* dst, size_t count, int dtype_in,
+                              int dtype_comm, int dtype_out, int op, int algo, int64_t* plan);
 
 /* dst[r*bytes_per_rank ...] = src of rank r (rank order, graph.py:575-579). */
 RP_API int rp_all_gather(rp_comm_t comm, const void* src, void* dst, size_t bytes_per_rank, void* stream);

@@ -82,6 +82,7 @@ SIGNATURES = {
                                    _c_void_p]),
     "rp_all_reduce_algo": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _i, _i, _i,
                                 ctypes.POINTER(ctypes.c_int)]),
+    "rp_all_reduce_plan": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _i, _i, _i, _pi64]),
     "rp_all_reduce_v": (_i, [_c_void_p, _pp, _pp, _size_t, _i, _i, _i, _i, _i, _c_void_p]),
     "rp_all_gather_v": (_i, [_c_void_p, _pp, _pp, _size_t, _c_void_p]),
     "rp_broadcast_v": (_i, [_c_void_p, _pp, _pp, _size_t, _i, _i, _c_void_p]),

@@ -182,6 +182,20 @@ class _Base:
                    "all_reduce_algo")
         return {1: "oneshot", 2: "twoshot", 3: "nvls", 5: "flat"}[chosen.value]
 
+    def plan_for(self, x: torch.Tensor, kind: str = "sum", out: torch.Tensor | None = None,
+                 comm_dtype: torch.dtype | None = None, algo: str = "auto") -> tuple:
+        """(algorithm, push form, src pool offset or -1, dst pool offset or -1) that
+        all_reduce_tensor(x, kind, out, comm_dtype, algo) would follow (include/rp.h
+        rp_all_reduce_plan); every rank must agree on it. ``out=None``: a fresh
+        output, as all_reduce_tensor allocates."""
+        code = dtype_code(x.dtype)
+        ccode = dtype_code(comm_dtype) if comm_dtype is not None else code
+        optr, ocode = (0, code) if out is None else (out.data_ptr(), dtype_code(out.dtype))
+        plan, _keep = _lib.i64_array([0, 0, 0, 0])
+        _lib.check(self._lib.rp_all_reduce_plan(self._handle, x.data_ptr(), optr, x.numel(), code, ccode,
+                                                ocode, _op(kind), _algo(algo), plan), "all_reduce_plan")
+        return tuple(int(v) for v in _keep)
+
     # -- host buffers in, host buffer out ------------------------------------
     HOST_CHUNK_BYTES = 8 << 20
     HOST_RING = 3

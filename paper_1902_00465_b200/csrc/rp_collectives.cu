@@ -381,6 +381,25 @@ int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* ds
   return bytes <= oneshot_max ? RP_ALGO_ONESHOT : RP_ALGO_TWOSHOT;
 }
 
+// What rp_launch_all_reduce will do with these arguments, for cross-rank agreement
+// checks: every rank must pick the same algorithm, data-movement form and pool
+// placement (a rank passing a pool view where a peer passes a plain tensor would
+// launch a different kernel against the shared barrier state).
+void rp_plan_all_reduce(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
+                        int dtype_comm, int dtype_out, int op, int algo, int64_t* plan) {
+  const int a = rp_resolve_ar_algo(c, src, dst, count, dtype_in, dtype_comm, dtype_out, op, algo);
+  size_t so = 0, doff = 0;
+  const bool sp = symmetric_in_pool(c, src, count * rp_dtype_size(dtype_in), &so);
+  const bool dp = symmetric_in_pool(c, dst, count * rp_dtype_size(dtype_out), &doff);
+  int push = 0;
+  if (!c->is_virtual && a != RP_ALGO_NVLS) push = (a == RP_ALGO_ONESHOT || !(sp && dtype_in == dtype_comm)) ? 1 : 0;
+  if (const char* e = getenv("RP_AR_IMPL")) push = (e[0] == 'p' && e[1] == 'u' && e[2] == 's') ? 1 : 0;
+  plan[0] = a;
+  plan[1] = push;
+  plan[2] = sp ? (int64_t)so : -1;
+  plan[3] = dp ? (int64_t)doff : -1;
+}
+
 int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, size_t count,
                          int dtype_in, int dtype_comm, int dtype_out, int op, int algo,
                          cudaStream_t stream) {

@@ -668,6 +668,18 @@ int rp_all_reduce_algo(rp_comm_t c, const void* src, const void* dst, size_t cou
   return RP_OK;
 }
 
+int rp_all_reduce_plan(rp_comm_t c, const void* src, const void* dst, size_t count, int dtype_in, int dtype_comm,
+                       int dtype_out, int op, int algo, int64_t* plan) {
+  RP_REQUIRE_READY(c, "rp_all_reduce_plan");
+  if (!plan) return rp_fail(RP_ERR_INVALID, "rp_all_reduce_plan: NULL argument");
+  if (!rp_dtype_valid(dtype_in) || !rp_dtype_valid(dtype_comm) || !rp_dtype_valid(dtype_out))
+    return rp_fail(RP_ERR_INVALID, "rp_all_reduce_plan: unknown dtype");
+  const void* s[RP_MAX_RANKS] = {src};
+  const void* d[RP_MAX_RANKS] = {dst};
+  rp_plan_all_reduce(c, s, d, count, dtype_in, dtype_comm, dtype_out, op, algo, plan);
+  return RP_OK;
+}
+
 int rp_all_reduce_v(rp_comm_t c, const void* const* src, void* const* dst, size_t count, int dtype_in,
                     int dtype_comm, int dtype_out, int op, int algo, void* stream) {
   RP_REQUIRE_READY(c, "rp_all_reduce_v");

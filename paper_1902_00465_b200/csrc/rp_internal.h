@@ -216,6 +216,8 @@ bool rp_nvls_covers(rp_comm* c, const void* p, size_t bytes);
 // Algorithm rp_all_reduce runs (AUTO resolved): RP_ALGO_ONESHOT / TWOSHOT / NVLS
 int rp_resolve_ar_algo(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
                        int dtype_comm, int dtype_out, int op, int algo);
+void rp_plan_all_reduce(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
+                        int dtype_comm, int dtype_out, int op, int algo, int64_t* plan);
 int rp_relay_bcast_launch(rp_comm* c, const void* src, void* dst, size_t bytes, int root, bool land_in_dst,
                           size_t land_off, cudaStream_t stream,
                           int (*dyn)(rp_comm*, const void*, CollArgs&, cudaStream_t, const char*, int, int, uint32_t),

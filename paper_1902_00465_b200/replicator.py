@@ -434,13 +434,17 @@ class Replicator:
         self._call_index = 0
         self.comm.new_generation()
 
-    def _verify(self, label, kind, shape, dtype):
+    def _verify(self, label, kind, shape, dtype, plan=None):
         """check_protocol on a multi-process replicator: all ranks must be issuing
-        the same collective at the same position of the generation."""
+        the same collective at the same position of the generation -- and, for an
+        all-reduce, with the same plan (algorithm, data-movement form, pool
+        placement; include/rp.h rp_all_reduce_plan), since ranks that place their
+        buffers differently would launch different kernels."""
         if not self.check_protocol or self.is_virtual or self.comm.world == 1:
             return
         self.comm._use_label(label)
-        self.comm.verify(label, kind, shape, dtype, position=(self._generation, self._call_index))
+        self.comm.verify(label, kind if plan is None else (kind, plan), shape, dtype,
+                         position=(self._generation, self._call_index))
         self._call_index += 1
 
     def all_reduce(self, x: torch.Tensor, kind: str = "sum", label: str | None = None) -> torch.Tensor:
@@ -451,7 +455,8 @@ class Replicator:
             y = self._collective(("all_reduce", label, kind, tuple(x.shape), x.dtype), x.detach(),
                                  lambda xs: self.comm.all_reduce(xs, kind))
             return _novjp(x, y, f"all_reduce({kind})")
-        self._verify(label, kind, x.shape, x.dtype)
+        plan = self.comm.plan_for(x.detach(), kind) if self.check_protocol else None
+        self._verify(label, kind, x.shape, x.dtype, plan)
         return _AllReduceFn.apply(x, self.comm, kind)
 
     def all_sum(self, x: torch.Tensor, label: str | None = None) -> torch.Tensor:

@@ -682,6 +682,14 @@ def body_protocol(rank, world, env):
     except errors.ProtocolError as e:
         assert "issued" in str(e) and f"rank {rank}" in str(e), str(e)
     repl.new_generation()
+    # placement disagreement: rank 0 passes a pool view, the others a
+    # plain tensor -- different kernels against shared barrier state; caught by the
+    # plan digest (include/rp.h rp_all_reduce_plan) before anything launches
+    pooled = repl.comm.alloc(16, torch.float32)
+    z = pooled if rank == 0 else torch.zeros(16, device=dev)
+    with pytest.raises(errors.ProtocolError):
+        repl.all_sum(z, label="placed")
+    repl.new_generation()
     # the duck type (graph.py:575-579) with ragged leading dimensions; scalars stay scalars
     rows = torch.arange((rank + 1) * 3, dtype=torch.float32, device=dev).reshape(rank + 1, 3)
     got = repl.comm.all_gather(rows)
@@ -814,6 +822,50 @@ def body_overlap(rank, world, env):
         flat = torch.cat([p.reshape(-1) for p in results[2]])
         gl = env.all_gather_object(H(flat))
         assert all(EQ(t, gl[0]) for t in gl), "replicas diverged"
+
+
+def body_overlap_with_bn(rank, world, env):
+    """with overlap=True, bucket all-reduces run on a side stream
+    while backward issues its OWN collectives on the compute stream (the BN
+    backward exchange of CrossReplicaBatchNorm). Every kernel of a communicator
+    shares its device-side sequencing state, so they must not run concurrently:
+    Communicator._stream orders each launch after the previous one whatever the
+    stream. The overlapped run must give the same bits as the synchronous one."""
+    from paper_1902_00465_b200.replicator import CrossReplicaBatchNorm, Replicator
+
+    dev = env.dev
+    results = []
+    for overlap in (False, True):
+        repl = Replicator(device=env.device, bootstrap=env.bootstrap, pool_bytes=32 << 20,
+                          bucket_bytes=2048 if overlap else None)
+
+        def net():
+            return torch.nn.Sequential(torch.nn.Conv2d(3, 16, 3, padding=1), CrossReplicaBatchNorm(16, repl),
+                                       torch.nn.ReLU(), torch.nn.Conv2d(16, 16, 3, padding=1),
+                                       CrossReplicaBatchNorm(16, repl), torch.nn.ReLU(),
+                                       torch.nn.AdaptiveAvgPool2d(1), torch.nn.Flatten(), torch.nn.Linear(16, 10))
+
+        torch.manual_seed(rank)
+        with repl.context():
+            model = repl.replicate(lambda: net().to(memory_format=torch.channels_last))
+            opt = repl.wrap_optimizer(torch.optim.SGD(model.local.parameters(), lr=0.05), overlap=overlap)
+        if overlap:
+            assert len(opt.buckets) > 2
+        for step in range(3):
+            g = torch.Generator().manual_seed(100 * step + rank)
+            xb = torch.randn(8, 3, 10, 10, generator=g).to(dev).contiguous(memory_format=torch.channels_last)
+            yb = torch.randint(0, 10, (8,), generator=g).to(dev)
+            opt.zero_grad()
+            torch.nn.functional.cross_entropy(model.local(xb), yb).backward()
+            opt.step()
+        env.sync()
+        results.append([H(p.detach()) for p in model.local.parameters()])
+        if overlap:
+            opt.remove_hooks()
+        repl.comm.check()
+        repl.comm.close()
+    for a, b in zip(*results):
+        assert torch.equal(a, b), "overlapped exchange beside BN collectives differs from the synchronous one"
 
 
 def body_host_pipeline(rank, world, env):

@@ -172,6 +172,12 @@ def test_overlapped_wrap_optimizer_loopback(world):
 
 @pytest.mark.timeout(300)
 @W24
+def test_overlap_beside_bn_collectives_loopback(world):
+    run_loopback("body_overlap_with_bn", world)
+
+
+@pytest.mark.timeout(300)
+@W24
 def test_host_pipelined_all_reduce_loopback(world):
     run_loopback("body_host_pipeline", world)
 

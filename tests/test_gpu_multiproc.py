@@ -125,6 +125,10 @@ def test_overlapped_wrap_optimizer_multiprocess():
     run_world("body_overlap")
 
 
+def test_overlap_beside_bn_collectives_multiprocess():
+    run_world("body_overlap_with_bn")
+
+
 def test_host_pipelined_all_reduce_multiprocess():
     run_world("body_host_pipeline")
 
