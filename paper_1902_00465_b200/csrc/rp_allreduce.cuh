@@ -526,6 +526,148 @@ __global__ void __launch_bounds__(kThreads, 1) ar_virtual_flat(const CollArgs a)
 }
 
 // ---------------------------------------------------------------------------
+// K2v-bulk: the same flat fold with the operands staged by the bulk-copy engine
+// (cp.async.bulk global->shared, completion counted on an mbarrier) instead of
+// 16-byte register loads -- the Blackwell data-movement path, A/B against the
+// register form (RP_VFLAT_BULK=1). Every warp runs its own 2-stage ring: lane 0
+// arms the stage's mbarrier with the byte count and issues NR bulk copies of one
+// 32*kBulkU-vector slice each; the warp waits on the phase, folds from shared
+// memory (lane-contiguous 16-byte reads, conflict-free) and stores the result to
+// all NR outputs; meanwhile the next stage's copies are in flight. Bytes in flight
+// no longer cost registers. Only the whole, 16-byte-aligned vectors go through the
+// bulk engine (the host checks alignment and that no cast is fused); a partial
+// last vector is folded by one warp on the register path, so no copy ever reads
+// past a buffer's end.
+// ---------------------------------------------------------------------------
+constexpr int kBulkThreads = 256;
+constexpr int kBulkU = 2;                     // 16-byte packets per lane per operand per stage
+constexpr int kBulkSlice = 32 * kBulkU;       // vectors per operand slice
+constexpr int kBulkStages = 2;
+__host__ __device__ constexpr size_t bulk_smem_bytes(int nr) {
+  return (size_t)(kBulkThreads / 32) * kBulkStages * nr * kBulkSlice * 16;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "RP_MBAR_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra RP_MBAR_DONE;\n"
+      "bra RP_MBAR_WAIT;\n"
+      "RP_MBAR_DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int DT, int OP, int NR>
+__global__ void __launch_bounds__(kBulkThreads, 1) ar_virtual_flat_bulk(const CollArgs a) {
+  using T = typename DType<DT>::T;
+  using A = typename DType<DT>::Acc;
+  constexpr int VEC = 16 / sizeof(T);
+  extern __shared__ __align__(128) uint4 ring[];  // [warp][stage][NR][kBulkSlice]
+  __shared__ __align__(8) uint64_t bars[kBulkThreads / 32][kBulkStages];
+  if (rp_aborted(a.t, 0)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t Vfull = a.count / VEC;  // whole vectors: every byte of them lies inside the buffers
+  const uint32_t tv = a.tile_v;
+  const uint32_t ntiles = (uint32_t)((Vfull + tv - 1) / tv);
+  uint32_t* ctr = a.t.sig[0] + RP_ST_VFLAT_CTR;
+  uint4* mine = ring + (size_t)warp * kBulkStages * NR * kBulkSlice;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // the partial last vector (count % VEC elements): one warp, register path
+  if (blockIdx.x == 0 && warp == 0 && Vfull * VEC < a.count && lane == 0) {
+    uint4 x[NR];
+#pragma unroll
+    for (int p = 0; p < NR; ++p) x[p] = load_src<T>(a, a.src[p], Vfull, false);
+    const uint4 r = fold_packet<T, A, OP, NR>(x);
+#pragma unroll
+    for (int p = 0; p < NR; ++p) store_dst<T>(a, a.dst[p], Vfull, false, r);
+  }
+  // warp-uniform producer state: the next slice to issue
+  uint32_t tile = claim_ctr(ctr);
+  size_t nxt = (size_t)tile * tv;
+  size_t tile_hi = tile < ntiles ? std::min(nxt + tv, Vfull) : 0;
+  size_t st_v0[kBulkStages];
+  uint32_t st_n[kBulkStages];
+  uint32_t parity = 0;  // bit s: phase of stage s
+  int inflight = 0, s_issue = 0, s_cons = 0;
+  auto issue = [&]() {  // one slice of the current tile into stage s_issue (tile < ntiles)
+    const uint32_t n = (uint32_t)std::min<size_t>(kBulkSlice, tile_hi - nxt);
+    st_v0[s_issue] = nxt;
+    st_n[s_issue] = n;
+    if (lane == 0) {
+      uint64_t* bar = &bars[warp][s_issue];
+      mbar_arrive_expect_tx(bar, n * 16u * NR);
+#pragma unroll
+      for (int p = 0; p < NR; ++p)
+        bulk_g2s(mine + ((size_t)s_issue * NR + p) * kBulkSlice, (const char*)a.src[p] + nxt * 16, n * 16u, bar);
+    }
+    nxt += n;
+    if (nxt >= tile_hi) {  // next tile
+      tile = claim_ctr(ctr);
+      nxt = (size_t)tile * tv;
+      tile_hi = tile < ntiles ? std::min(nxt + tv, Vfull) : 0;
+    }
+    s_issue ^= 1;
+    ++inflight;
+  };
+  while (true) {
+    while (inflight < kBulkStages && tile < ntiles) issue();
+    if (inflight == 0) break;
+    mbar_wait(&bars[warp][s_cons], (parity >> s_cons) & 1u);
+    parity ^= 1u << s_cons;
+    const uint4* stage = mine + (size_t)s_cons * NR * kBulkSlice;
+    const size_t v0 = st_v0[s_cons];
+    const uint32_t n = st_n[s_cons];
+#pragma unroll
+    for (int u = 0; u < kBulkU; ++u) {
+      const uint32_t i = lane + 32u * u;
+      if (i < n) {
+        uint4 x[NR];
+#pragma unroll
+        for (int p = 0; p < NR; ++p) x[p] = stage[(size_t)p * kBulkSlice + i];
+        const uint4 r = fold_packet<T, A, OP, NR>(x);
+#pragma unroll
+        for (int p = 0; p < NR; ++p) st128((char*)a.dst[p] + (v0 + i) * 16, r);
+      }
+    }
+    __syncwarp();  // every lane's reads of this stage precede its refill
+    s_cons ^= 1;
+    --inflight;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.t.sig[0] + RP_ST_VFLAT_DONE, 1u) == gridDim.x - 1) {
+      state_store(a.t, 0, RP_ST_VFLAT_CTR, 0u);
+      state_store(a.t, 0, RP_ST_VFLAT_DONE, 0u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // world == 1: local op (identity fold) with the same conversion rules
 // ---------------------------------------------------------------------------
 template <int DT, int OP>
@@ -566,6 +708,18 @@ const void* pick_ar(int algo, int world, int push) {
                                      : (const void*)ar_twoshot_dyn<DT, OP, NR, true>;           \
     return algo == RP_ALGO_ONESHOT ? (const void*)ar_oneshot<DT, OP, NR>                        \
                                    : (const void*)ar_twoshot_dyn<DT, OP, NR, false>;
+  if (algo == RP_ALGO_FLAT + 100) {  // bulk-copy form of the flat kernel
+    switch (world) {
+      case 2: return (const void*)ar_virtual_flat_bulk<DT, OP, 2>;
+      case 3: return (const void*)ar_virtual_flat_bulk<DT, OP, 3>;
+      case 4: return (const void*)ar_virtual_flat_bulk<DT, OP, 4>;
+      case 5: return (const void*)ar_virtual_flat_bulk<DT, OP, 5>;
+      case 6: return (const void*)ar_virtual_flat_bulk<DT, OP, 6>;
+      case 7: return (const void*)ar_virtual_flat_bulk<DT, OP, 7>;
+      case 8: return (const void*)ar_virtual_flat_bulk<DT, OP, 8>;
+      default: return nullptr;
+    }
+  }
   if (algo == RP_ALGO_FLAT) {
     switch (world) {
       case 2: return (const void*)ar_virtual_flat<DT, OP, 2>;

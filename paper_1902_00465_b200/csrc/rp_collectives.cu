@@ -27,6 +27,8 @@ const void* rp_pick_ar_f32(int op, int algo, int world, int push);
 const void* rp_pick_ar_f64(int op, int algo, int world, int push);
 const void* rp_pick_ar_bf16(int op, int algo, int world, int push);
 const void* rp_pick_ar_f16(int op, int algo, int world, int push);
+size_t rp_bulk_smem_bytes(int nr);
+int rp_bulk_threads();
 
 static const void* pick_ar_any(int dtype, int op, int algo, int world, int push) {
   switch (dtype) {
@@ -451,6 +453,29 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
   }
   if (algo == RP_ALGO_FLAT) {
     if (!c->is_virtual) return rp_fail(RP_ERR_INVALID, "all_reduce(flat): needs a virtual communicator");
+    // A/B: the bulk-copy (cp.async.bulk + mbarrier) staging of the same fold, for
+    // aligned buffers without a fused cast
+    if (const char* be = getenv("RP_VFLAT_BULK")) {
+      bool ok = be[0] == '1' && dtype_in == dtype_comm && dtype_out == dtype_comm;
+      for (int i = 0; i < W && ok; ++i) ok = ((((uintptr_t)src[i]) | ((uintptr_t)dst[i])) & 15u) == 0;
+      if (ok) {
+        const void* fb = pick_ar_any(dtype_comm, op, RP_ALGO_FLAT + 100, W, 0);
+        if (!fb) return rp_fail(RP_ERR_INVALID, "all_reduce(flat bulk): unsupported replica count (2..8)");
+        const size_t smem = rp_bulk_smem_bytes(W);
+        RP_CUDA_CHECK(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fb, rp_bulk_threads(), smem) != cudaSuccess || occ < 1)
+          occ = 1;
+        int blocks = occ * c->num_sms;
+        if (c->cap() > 0) blocks = std::min(blocks, c->cap());
+        const size_t warps = (size_t)blocks * (rp_bulk_threads() / 32);
+        size_t tv = V / (warps * 4);
+        if (const char* e = getenv("RP_VFLAT_TILE")) tv = (size_t)atoi(e);
+        a.tile_v = (uint32_t)std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
+        void* args[] = {&a};
+        return rp_launch(c, fb, dim3(std::max(blocks, 1)), dim3(rp_bulk_threads()), args, smem, stream, false);
+      }
+    }
     const void* fn = pick_ar_any(dtype_comm, op, RP_ALGO_FLAT, W, 0);
     if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce(flat): unsupported replica count (2..8)");
     // one co-resident wave on EVERY SM; tiles of 256..4096 vectors, >= 4 per warp
