@@ -458,10 +458,9 @@ __global__ void __launch_bounds__(kBnThreads) bn_stats_fused(const FusedBnArgs f
     uint32_t* ctr = f.e.t.sig[rank] + RP_ST_BN_GRID_CTR;
     __threadfence();
     atomicAdd(ctr, 1u);
-    uint32_t v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    } while ((int32_t)(v - (base + total)) < 0);
+    // bounded like every other wait: a grid that could not become co-resident
+    // aborts (rp_comm_check reports it) instead of spinning forever
+    wait_reach(f.e.t, f.e.world, f.e.timeout_ns, rank, ctr, base + total);
   }
   __syncthreads();
   if ((int)bid >= f.ex_blocks || rp_aborted(f.e.t, rank)) return;

@@ -1,4 +1,6 @@
-"""Debug: random sequence of collectives in a loopback world, each checked."""
+"""Debug: random sequence of collectives in a loopback world (W ranks on one GPU), each
+checked against the oracle. PINNED=1 copies results through pinned memory (the
+product path, comm.to_host); CHECK=1 adds comm.check() after every op."""
 import os, sys
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")
 import numpy as np
@@ -33,7 +35,7 @@ def body(rank):
         h.copy_(t.reshape(-1), non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return h.numpy().copy().reshape(t.shape)
-    comm = Communicator(device=0, bootstrap=lw.bootstrap(rank), pool_bytes=POOL, timeout_s=5)
+    comm = Communicator(device=0, bootstrap=lw.bootstrap(rank), pool_bytes=POOL, timeout_s=float(os.environ.get("TMO", "5")))
     bucket = comm.alloc(300000, torch.float32)
     log = []
     import time
@@ -82,3 +84,4 @@ for r, log in enumerate(out):
             nbad += 1
             print("rank", r, row, flush=True)
 print("bad rows:", nbad)
+sys.exit(1 if nbad else 0)
