@@ -436,12 +436,26 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
   const bool sync = a.world > 1;
   if (sync && !bn_barrier(a, rank, nblk, seen + 1u)) return;
   if (lane == 0 && c < C) {
+    // every rank's record is requested before any is added (one NVLink round trip,
+    // not world of them), then folded in ascending rank order
+    double r0[RP_MAX_RANKS], r1[RP_MAX_RANKS], r2[RP_MAX_RANKS];
+#pragma unroll
+    for (int p = 0; p < RP_MAX_RANKS; ++p) {
+      if (p < a.world) {
+        const double* rec = (const double*)(a.t.data[p] + bn_off) + c * 3;
+        r0[p] = rec[0];
+        r1[p] = rec[1];
+        r2[p] = rec[2];
+      }
+    }
     double A1 = 0.0, A2 = 0.0, Mt = 0.0;
-    for (int p = 0; p < a.world; ++p) {  // ascending rank order
-      const double* rec = (const double*)(a.t.data[p] + bn_off) + c * 3;
-      A1 += rec[0];
-      A2 += rec[1];
-      Mt += rec[2];
+#pragma unroll
+    for (int p = 0; p < RP_MAX_RANKS; ++p) {
+      if (p < a.world) {
+        A1 += r0[p];
+        A2 += r1[p];
+        Mt += r2[p];
+      }
     }
     if (a.bwd) {
       a.out0[rep][c] = (float)A1;

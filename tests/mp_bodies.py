@@ -643,6 +643,7 @@ def body_fused_apply(rank, world, env):
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, capture_error_mode="thread_local"):
         train_step()
+    env.barrier()  # nobody replays (real launches) while a peer is still inside capture's device sync
     before = flat.clone()
     for _ in range(3):
         graph.replay()
@@ -730,6 +731,7 @@ def body_graph(rank, world, env):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, capture_error_mode="thread_local"):
         seq()
+    env.barrier()  # nobody replays (real launches) while a peer is still inside capture's device sync
     for it in range(5):
         xs_s = _inputs(world, 5000, seed=1000 + it)
         xs_b = _inputs(world, 3 << 20, seed=2000 + it)
