@@ -812,6 +812,12 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
     const int64_t wave = rp_wave_per_rank(c, fper);  // co-resident blocks per replica
     if ((int64_t)grid.x * grid.y > wave) grid.y = (unsigned)std::max<int64_t>(1, wave / grid.x);
     const int64_t emax = std::min<int64_t>(RP_BN_ROWS, wave);
+    // exchange blocks: as many as the partial pass's grid already has (never more
+    // splits than the local pass wants: a 4 MiB layer at 64 splits would otherwise
+    // be cut into 256 splits of 4 rows -- 4x the partial traffic and the fold work),
+    // unless C needs more blocks even at 256 channels per block
+    const int64_t egrid = std::min<int64_t>(emax, (int64_t)grid.x * grid.y);
+    while (fcpb < kExThreads && (ch + fcpb - 1) / fcpb > egrid) fcpb *= 2;
     while (fcpb < kExThreads && (ch + fcpb - 1) / fcpb > emax) fcpb *= 2;
     fex = (int)((ch + fcpb - 1) / fcpb);
     if ((int64_t)grid.x * grid.y < fex) grid.y = (unsigned)((fex + grid.x - 1) / grid.x);  // empty splits: zeros
