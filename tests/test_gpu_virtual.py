@@ -267,10 +267,12 @@ def test_collectives_replay_in_cuda_graph(n, impl):
     o_big = [torch.empty_like(t) for t in big]
     o_gat = [torch.empty(n, 777, device=DEV) for _ in range(n)]
     o_bc = [torch.empty_like(t) for t in gat]
+    o_flat = [torch.empty_like(t) for t in big]
 
     def seq():
         comm.all_reduce(small, "sum", outs=o_small, algo="oneshot")
         comm.all_reduce(big, "premean", outs=o_big, algo="twoshot")
+        comm.all_reduce(big, "max", outs=o_flat, algo="flat")  # claim counters reset by its last block
         comm.all_gather(gat, outs=o_gat)
         comm.broadcast(gat, root=n - 1, outs=o_bc)
 
@@ -294,6 +296,7 @@ def test_collectives_replay_in_cuda_graph(n, impl):
         for r in range(n):
             assert host(o_small[r]).tobytes() == O.fold_sum(vals[0]).tobytes(), it
             assert host(o_big[r]).tobytes() == O.fold_premean(vals[1]).tobytes(), it
+            assert host(o_flat[r]).tobytes() == O.fold_max(vals[1]).tobytes(), it
             assert host(o_gat[r]).tobytes() == np.concatenate(vals[2]).tobytes(), it
             assert host(o_bc[r]).tobytes() == vals[2][n - 1].tobytes(), it
     comm.check()
