@@ -271,6 +271,7 @@ def run_ours(args, rank, world, local):
             comm.all_reduce_tensor(buf, args.kind, out=buf, algo=args.algo)
 
         args.chosen_algo = comm.algorithm_for(buf, args.kind, out=buf, algo=args.algo)
+        args.topology = comm.topology()
 
     align = None
     if world > 1:
@@ -347,6 +348,7 @@ def run_ours(args, rank, world, local):
                     "link_gbs_per_direction": link_bytes / (ms / 1e3) / 1e9, "kernel": kernel}
         if getattr(args, "nvls_error", None):
             roofline["nvls_unavailable"] = args.nvls_error
+        roofline["topology_rank0"] = getattr(args, "topology", None)
 
     # e2e: host pinned buffers -> device -> all_reduce -> host, through the public API
     e2e = run_e2e(args, comm, world, n, count, dev, stream)

@@ -114,7 +114,8 @@ RP_API int rp_comm_export(rp_comm_t comm, void* buf, size_t* len);
  * (replaces the reference's MultiGpu device assignment): every
  * peer's GPU must be visible, CUDA peer access must work, and NVML must report
  * NVLink P2P to it (NVSwitch gives every pair NVLink) -- rp_topology_check's
- * policy; RP_ERR_CONFIG (-> ConfigurationError, errors.py:32) otherwise, naming
+ * policy -- and every rank's GPU must have the same number of active NVLink links
+ * (rp_topology_uniform); RP_ERR_CONFIG (-> ConfigurationError, errors.py:32) otherwise, naming
  * the pair and the link found. RP_ALLOW_PCIE=1 in the environment accepts PCIe
  * peer access (tests only). Then opens every peer's pool over CUDA IPC (loopback
  * peers: the plain pointer). */
@@ -136,6 +137,18 @@ enum {
  * allow_pcie; LOOPBACK only in a loopback world. RP_ERR_CONFIG with the offending
  * pair in rp_last_error() otherwise. Pure host logic (no device needed). */
 RP_API int rp_topology_check(int world, int rank, const int* links, int allow_pcie, int loopback);
+
+/* Uniformity of the NVLink fabric rp_comm_import also requires (unless
+ * RP_ALLOW_PCIE=1): every rank's GPU has the same number of active NVLink links
+ * (nvlinks[p], from NVML; -1 = unknown, skipped) and none has zero -- what an
+ * NVSwitch all-to-all gives (18 links per B200). RP_ERR_CONFIG otherwise, naming
+ * the ranks. Pure host logic. */
+RP_API int rp_topology_uniform(int world, const int* nvlinks);
+
+/* The topology rp_comm_import discovered: links[p] (RP_LINK_* from this rank to
+ * rank p) and nvlinks[p] (active NVLink links of rank p's GPU, -1 unknown), world
+ * entries each. */
+RP_API int rp_comm_topology(rp_comm_t comm, int* links, int* nvlinks);
 
 /* Loopback world (testing the multi-process kernels on ONE GPU): `world`
  * non-virtual communicators created in ONE process on the same device, each

@@ -64,6 +64,8 @@ SIGNATURES = {
     "rp_comm_set_loopback": (_i, [_c_void_p, _i]),
     "rp_loopback_prepare": (_i, [_i]),
     "rp_topology_check": (_i, [_i, _i, ctypes.POINTER(_i), _i, _i]),
+    "rp_topology_uniform": (_i, [_i, ctypes.POINTER(_i)]),
+    "rp_comm_topology": (_i, [_c_void_p, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "rp_comm_destroy": (_i, [_c_void_p]),
     "rp_comm_pool": (_i, [_c_void_p, _i, _pp, ctypes.POINTER(_size_t)]),
     "rp_comm_info": (_i, [_c_void_p, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i),

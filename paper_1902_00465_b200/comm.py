@@ -353,6 +353,17 @@ class Communicator(_Base):
     def num_replicas(self) -> int:
         return self.world
 
+    _LINK_NAMES = {0: "self", 1: "nvlink", 2: "pcie", 3: "none", 4: "unknown", 5: "same_device", 6: "loopback"}
+
+    def topology(self) -> dict:
+        """What rp_comm_import discovered (include/rp.h rp_comm_topology): the link
+        kind from this rank to every rank and every rank's active NVLink links."""
+        links = (ctypes.c_int * self.world)()
+        nvl = (ctypes.c_int * self.world)()
+        _lib.check(self._lib.rp_comm_topology(self._handle, links, nvl), "comm_topology")
+        return {"rank": self.rank, "links": [self._LINK_NAMES.get(v, str(v)) for v in links],
+                "nvlinks": list(nvl)}
+
     # -- zero-copy buffers --------------------------------------------------
     def alloc(self, numel: int, dtype: torch.dtype) -> torch.Tensor:
         """Tensor inside this rank's registered pool (exchanged without staging)."""

@@ -207,49 +207,67 @@ static int pack_common(bool pack, void* flat, int dtype_flat, const void* const*
 // topology discovery
 // ---------------------------------------------------------------------------
 
-// NVML, loaded at run time (no link-time dependency): NVLink P2P status of a pair.
-// Returns 1 (NVLink P2P), 0 (no NVLink between them) or -1 (NVML unavailable).
-static int nvml_nvlink_p2p(int dev_a, int dev_b, std::string* why) {
+// NVML, loaded at run time (no link-time dependency).
+typedef nvmlReturn_t (*nvml_by_pci_t)(const char*, nvmlDevice_t*);
+typedef nvmlReturn_t (*nvml_p2p_t)(nvmlDevice_t, nvmlDevice_t, nvmlGpuP2PCapsIndex_t, nvmlGpuP2PStatus_t*);
+typedef nvmlReturn_t (*nvml_link_state_t)(nvmlDevice_t, unsigned int, nvmlEnableState_t*);
+struct NvmlApi {
+  nvml_by_pci_t by_pci = nullptr;
+  nvml_p2p_t p2p = nullptr;
+  nvml_link_state_t link_state = nullptr;
+};
+static const NvmlApi& nvml() {
   static std::mutex mu;
-  static void* h = nullptr;
+  static NvmlApi api;
   static bool tried = false;
-  typedef nvmlReturn_t (*init_t)(void);
-  typedef nvmlReturn_t (*by_pci_t)(const char*, nvmlDevice_t*);
-  typedef nvmlReturn_t (*p2p_t)(nvmlDevice_t, nvmlDevice_t, nvmlGpuP2PCapsIndex_t, nvmlGpuP2PStatus_t*);
-  static by_pci_t by_pci = nullptr;
-  static p2p_t p2p = nullptr;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    if (!tried) {
-      tried = true;
-      h = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
-      if (h) {
-        init_t init = (init_t)dlsym(h, "nvmlInit_v2");
-        by_pci = (by_pci_t)dlsym(h, "nvmlDeviceGetHandleByPciBusId_v2");
-        p2p = (p2p_t)dlsym(h, "nvmlDeviceGetP2PStatus");
-        if (!init || !by_pci || !p2p || init() != NVML_SUCCESS) by_pci = nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!tried) {
+    tried = true;
+    if (void* h = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL)) {
+      typedef nvmlReturn_t (*init_t)(void);
+      init_t init = (init_t)dlsym(h, "nvmlInit_v2");
+      if (init && init() == NVML_SUCCESS) {
+        api.by_pci = (nvml_by_pci_t)dlsym(h, "nvmlDeviceGetHandleByPciBusId_v2");
+        api.p2p = (nvml_p2p_t)dlsym(h, "nvmlDeviceGetP2PStatus");
+        api.link_state = (nvml_link_state_t)dlsym(h, "nvmlDeviceGetNvLinkState");
       }
     }
   }
-  if (!by_pci || !p2p) {
+  return api;
+}
+static bool nvml_device(int dev, nvmlDevice_t* out) {
+  char bus[32];
+  return nvml().by_pci && cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) == cudaSuccess &&
+         nvml().by_pci(bus, out) == NVML_SUCCESS;
+}
+
+// NVLink P2P status of a pair: 1 (NVLink P2P), 0 (no NVLink between them) or -1
+// (NVML unavailable).
+static int nvml_nvlink_p2p(int dev_a, int dev_b, std::string* why) {
+  nvmlDevice_t na, nb;
+  if (!nvml().p2p || !nvml_device(dev_a, &na) || !nvml_device(dev_b, &nb)) {
     *why = "NVML unavailable: cannot confirm NVLink";
     return -1;
   }
-  char bus_a[32], bus_b[32];
-  nvmlDevice_t na, nb;
-  if (cudaDeviceGetPCIBusId(bus_a, sizeof(bus_a), dev_a) != cudaSuccess ||
-      cudaDeviceGetPCIBusId(bus_b, sizeof(bus_b), dev_b) != cudaSuccess || by_pci(bus_a, &na) != NVML_SUCCESS ||
-      by_pci(bus_b, &nb) != NVML_SUCCESS) {
-    *why = "NVML cannot resolve the devices";
-    return -1;
-  }
   nvmlGpuP2PStatus_t st = NVML_P2P_STATUS_UNKNOWN;
-  if (p2p(na, nb, NVML_P2P_CAPS_INDEX_NVLINK, &st) != NVML_SUCCESS) {
+  if (nvml().p2p(na, nb, NVML_P2P_CAPS_INDEX_NVLINK, &st) != NVML_SUCCESS) {
     *why = "nvmlDeviceGetP2PStatus failed";
     return -1;
   }
   if (st != NVML_P2P_STATUS_OK) *why = "NVML reports no NVLink P2P (status " + std::to_string((int)st) + ")";
   return st == NVML_P2P_STATUS_OK ? 1 : 0;
+}
+
+// Active NVLink links of a device (an NVSwitch B200 has 18), -1 when unknown.
+static int nvml_active_links(int dev) {
+  nvmlDevice_t d;
+  if (!nvml().link_state || !nvml_device(dev, &d)) return -1;
+  int n = 0;
+  for (unsigned l = 0; l < NVML_NVLINK_MAX_LINKS; ++l) {
+    nvmlEnableState_t st = NVML_FEATURE_DISABLED;
+    if (nvml().link_state(d, l, &st) == NVML_SUCCESS && st == NVML_FEATURE_ENABLED) ++n;
+  }
+  return n;
 }
 
 // Link from this rank to peer `me_or_peer` (include/rp.h RP_LINK_*).
@@ -412,6 +430,7 @@ int rp_comm_export(rp_comm_t c, void* buf, size_t* len) {
   e.base = (uint64_t)(uintptr_t)c->alloc[c->rank];
   e.pid = (int32_t)getpid();
   e.loopback = c->loopback ? 1 : 0;
+  e.nvlinks = c->loopback ? -1 : nvml_active_links(c->device);
   memcpy(buf, &e, sizeof(e));
   *len = sizeof(e);
   return RP_OK;
@@ -462,10 +481,17 @@ int rp_comm_import(rp_comm_t c, const void* all, size_t len) {
   const char* pe = getenv("RP_ALLOW_PCIE");
   const int allow = (pe && pe[0] == '1') ? 1 : 0;
   int rc = rp_topology_check(c->world, c->rank, links, allow, c->loopback ? 1 : 0);
+  int nvl[RP_MAX_RANKS];
+  for (int p = 0; p < c->world; ++p) nvl[p] = ex[p].nvlinks;
+  if (!rc && !c->loopback && !allow) rc = rp_topology_uniform(c->world, nvl);
   if (rc) {
     for (int p = 0; p < c->world; ++p)
       if (!why[p].empty()) rp_set_error(rp_last_error() + std::string("; rank ") + std::to_string(p) + ": " + why[p]);
     return rc;
+  }
+  for (int p = 0; p < c->world; ++p) {
+    c->links[p] = links[p];
+    c->nvlinks[p] = nvl[p];
   }
   if (c->loopback) {
     for (int p = 0; p < c->world; ++p) lb_ref(p == c->rank ? c->alloc[c->rank] : (char*)(uintptr_t)ex[p].base);
@@ -506,6 +532,32 @@ int rp_loopback_prepare(int device) {
   for (cudaMemPool_t p : pools) {
     int off = 0;
     RP_CUDA_CHECK(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &off));
+  }
+  return RP_OK;
+}
+
+int rp_topology_uniform(int world, const int* nvlinks) {
+  if (!nvlinks || world < 1 || world > RP_MAX_RANKS) return rp_fail(RP_ERR_INVALID, "rp_topology_uniform: bad arguments");
+  for (int p = 0; p < world; ++p) {
+    if (nvlinks[p] < 0) continue;  // NVML could not count (the P2P check already required NVLink)
+    for (int q = 0; q < p; ++q) {
+      if (nvlinks[q] >= 0 && nvlinks[q] != nvlinks[p])
+        return rp_fail(RP_ERR_CONFIG, "topology: non-uniform NVLink -- rank " + std::to_string(q) + " has " +
+                                          std::to_string(nvlinks[q]) + " active links, rank " + std::to_string(p) +
+                                          " has " + std::to_string(nvlinks[p]) +
+                                          " (an NVSwitch all-to-all gives every GPU the same links)");
+    }
+    if (nvlinks[p] == 0)
+      return rp_fail(RP_ERR_CONFIG, "topology: rank " + std::to_string(p) + " has no active NVLink link");
+  }
+  return RP_OK;
+}
+
+int rp_comm_topology(rp_comm_t c, int* links, int* nvlinks) {
+  if (!c || !links || !nvlinks) return rp_fail(RP_ERR_INVALID, "rp_comm_topology: NULL argument");
+  for (int p = 0; p < c->world; ++p) {
+    links[p] = c->is_virtual ? RP_LINK_SELF : (c->world == 1 ? RP_LINK_SELF : c->links[p]);
+    nvlinks[p] = c->is_virtual || c->world == 1 ? -1 : c->nvlinks[p];
   }
   return RP_OK;
 }

@@ -99,6 +99,9 @@ struct rp_comm {
   bool loopback = false;
   int loopback_cap = 0;    // num_sms / world in a loopback world
   bool lb_refs = false;    // holds a reference on every rank's region (loopback registry)
+  // topology discovered by rp_comm_import (rp_comm_topology)
+  int links[RP_MAX_RANKS] = {};
+  int nvlinks[RP_MAX_RANKS] = {};
   // effective per-rank block cap (0: none): the caller's cap and the loopback cap
   int cap() const {
     if (loopback_cap > 0) return block_cap > 0 ? (block_cap < loopback_cap ? block_cap : loopback_cap) : loopback_cap;
@@ -132,6 +135,7 @@ struct RpExport {
   uint64_t base;     // region base in the exporting process (loopback peers only)
   int32_t pid;       // exporting process
   int32_t loopback;  // exporter runs a loopback world
+  int32_t nvlinks;   // active NVLink links of the exporter's GPU (NVML), -1 unknown
 };
 
 // Kernel argument block for the collectives (by value, < 4 KB).

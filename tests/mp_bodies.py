@@ -309,6 +309,49 @@ def body_reference_graph(rank, world, env):
     comm.close()
 
 
+def body_random_sequence(rank, world, env):
+    """SURVEY §5 flag-protocol test: a seeded random sequence of mixed collectives
+    (all-reduce of user / in-place / pool buffers, all_gather, broadcast from
+    varying roots; 1 to 262144 elements, so one-shot, two-shot, push and pull forms
+    and the landing-zone parities interleave) issued back to back with NO
+    synchronisation between calls, every result checked bit-exactly afterwards:
+    back-to-back collectives never read stale or overwritten peer data."""
+    from oracle import collectives as O
+    from paper_1902_00465_b200.comm import Communicator
+
+    dev = env.dev
+    rng = np.random.default_rng(2024)
+    ops = [(str(rng.choice(["ar", "ar_inplace", "ar_pool", "ag", "bc"])),
+            int(rng.choice([1, 7, 1000, 4097, 65536, 203530, 262144]))) for _ in range(48)]
+    comm = Communicator(device=env.device, bootstrap=env.bootstrap, pool_bytes=32 << 20)
+    bucket = comm.alloc(300000, torch.float32)
+    pending = []
+    for i, (op, count) in enumerate(ops):
+        xs = _cached(("seq", world, i, count), lambda: [np.random.default_rng(1000 * i + r).standard_normal(count)
+                                                        .astype(np.float32) for r in range(world)])
+        x = torch.from_numpy(xs[rank]).to(dev)
+        if op == "ar":
+            pending.append((i, op, comm.all_reduce_tensor(x, "sum"), O.fold_sum(xs)))
+        elif op == "ar_inplace":
+            comm.all_reduce_tensor(x, "sum", out=x)
+            pending.append((i, op, x, O.fold_sum(xs)))
+        elif op == "ar_pool":
+            b = bucket[:count]
+            b.copy_(x)
+            comm.all_reduce_tensor(b, "premean", out=b)
+            pending.append((i, op, b.clone(), O.fold_premean(xs)))  # the bucket is reused by later ops
+        elif op == "ag":
+            pending.append((i, op, comm.all_gather_tensor(x).reshape(-1), np.concatenate(xs)))
+        else:
+            comm.broadcast_tensor(x, root=i % world)
+            pending.append((i, op, x, xs[i % world]))
+    env.sync()
+    for i, op, got, want in pending:
+        assert H(got).numpy().tobytes() == want.tobytes(), (i, op, ops[i])
+    comm.check()
+    comm.close()
+
+
 def body_bn(rank, world, env):
     from oracle import collectives as O
     from paper_1902_00465_b200.replicator import CrossReplicaBatchNorm, Replicator

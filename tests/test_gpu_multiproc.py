@@ -81,6 +81,10 @@ def test_reference_graph_evaluate_through_communicator_multiprocess():
     run_world("body_reference_graph")
 
 
+def test_back_to_back_random_sequence_multiprocess():
+    run_world("body_random_sequence")
+
+
 def test_cross_replica_bn_autograd_multiprocess():
     run_world("body_bn")
 

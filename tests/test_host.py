@@ -309,6 +309,18 @@ def test_topology_policy_requires_nvlink_everywhere():
         _lib.check(lib.rp_topology_check(9, 0, _links(*([NV] * 9)), 0, 0))
 
 
+def test_topology_requires_uniform_nvlink():
+    """rp_comm_import also requires every GPU to have the same number of active NVLink
+    links (an NVSwitch all-to-all: 18 per B200); unknown counts (-1) are skipped."""
+    lib = _lib.load()
+    _lib.check(lib.rp_topology_uniform(4, _links(18, 18, 18, 18)))
+    _lib.check(lib.rp_topology_uniform(3, _links(18, -1, 18)))
+    with pytest.raises(errors.ConfigurationError, match="non-uniform NVLink"):
+        _lib.check(lib.rp_topology_uniform(4, _links(18, 18, 12, 18)), "comm_import")
+    with pytest.raises(errors.ConfigurationError, match="no active NVLink"):
+        _lib.check(lib.rp_topology_uniform(2, _links(0, 0)), "comm_import")
+
+
 # --- loopback bootstrap (bootstrap.py) ------------------------------------------
 
 def test_loopback_bootstrap_exchanges_in_rank_order():
