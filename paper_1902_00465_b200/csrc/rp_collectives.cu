@@ -469,7 +469,7 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
         int blocks = occ * c->num_sms;
         if (c->cap() > 0) blocks = std::min(blocks, c->cap());
         const size_t warps = (size_t)blocks * (rp_bulk_threads() / 32);
-        size_t tv = V / (warps * 4);
+        size_t tv = V / (warps * 8);  // ~8 tiles per warp: the tail is one small tile
         if (const char* e = getenv("RP_VFLAT_TILE")) tv = (size_t)atoi(e);
         a.tile_v = (uint32_t)std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
         void* args[] = {&a};
@@ -478,14 +478,14 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
     }
     const void* fn = pick_ar_any(dtype_comm, op, RP_ALGO_FLAT, W, 0);
     if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce(flat): unsupported replica count (2..8)");
-    // one co-resident wave on EVERY SM; tiles of 256..4096 vectors, >= 4 per warp
+    // one co-resident wave on EVERY SM; tiles of 256..4096 vectors
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
     int blocks = (int)std::min<size_t>((size_t)occ * c->num_sms, (V + 31) / 32);
     if (c->cap() > 0) blocks = std::min(blocks, c->cap());
     blocks = std::max(blocks, 1);
     const size_t warps = (size_t)blocks * (kThreads / 32);
-    size_t tv = V / (warps * 4);
+    size_t tv = V / (warps * 8);  // ~8 tiles per warp: the tail is one small tile
     if (const char* e = getenv("RP_VFLAT_TILE")) tv = (size_t)atoi(e);
     a.tile_v = (uint32_t)std::min<size_t>(std::max<size_t>(round_up(tv, 256), 256), 4096);
     return launch_coll(c, fn, dim3(blocks), a, stream, "virtual_flat", kThreads, /*coop=*/false);
