@@ -377,52 +377,15 @@ __device__ __forceinline__ bool bn_barrier(const ExArgs& a, int rank, int nblk, 
   return phase_wait(a.t, a.world, a.timeout_ns, rank, RP_BN_PHASE, target);
 }
 
-__device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk, int nblk) {
-  __shared__ double red[kExThreads][2];
-  // BN calls completed so far (one barrier each, equal on every rank); the record
-  // set alternates with its parity, so the next call can write its records while a
-  // slow peer may still be reading this one's: a rank reuses a set only after the
-  // following call's barrier, which every peer reaches after its reads
-  const uint32_t seen = state_load(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE);
+// The rank-level part of a statistics call, for channel c whose local sums (s1, s2)
+// this thread owns (owner): publish the record, meet the peers once (hierarchical
+// barrier over the nblk blocks of every rank), fold every rank's record in rank
+// order and write the outputs; advance the call count.
+__device__ __forceinline__ void finish_exchange(const ExArgs& a, int rank, int blk, int nblk, uint32_t seen,
+                                                int64_t c, bool owner, double s1, double s2) {
   const size_t bn_off = a.bn_off + (size_t)(seen & 1u) * RP_BN_HALF;
   const int rep = a.rank >= 0 ? 0 : rank;  // local replica index
-  const int tpc = kExThreads / a.cpb;      // threads per channel
-  const int lane = threadIdx.x % tpc;
-  const int64_t c = (int64_t)blk * a.cpb + threadIdx.x / tpc;
-  const int64_t C = a.C;
-  // fold the S split partials of channel c: thread `lane` of the channel's tpc
-  // threads sums splits lane, lane + tpc, ...; the tpc sums are then combined by a
-  // fixed shuffle tree (warp) and a fixed-order pass over warp sums -- deterministic,
-  // and log-depth (a serial pass over 256 values cost ~4 us at C = 128)
-  double s1 = 0.0, s2 = 0.0;
-  if (c < C) {
-    const double* P = a.part[rep];
-#pragma unroll 4
-    for (int s = lane; s < a.S; s += tpc) {
-      s1 += P[((int64_t)s * C + c) * 2];
-      s2 += P[((int64_t)s * C + c) * 2 + 1];
-    }
-  }
-  const int width = tpc < 32 ? tpc : 32;
-  for (int o = width >> 1; o > 0; o >>= 1) {
-    s1 += __shfl_down_sync(0xffffffffu, s1, o, width);
-    s2 += __shfl_down_sync(0xffffffffu, s2, o, width);
-  }
-  if (tpc > 32) {  // one partial per warp, folded in warp order by the channel's first thread
-    if ((threadIdx.x & 31) == 0) {
-      red[threadIdx.x >> 5][0] = s1;
-      red[threadIdx.x >> 5][1] = s2;
-    }
-    __syncthreads();
-    if (lane == 0) {
-      const int w0 = threadIdx.x >> 5;
-      for (int w = 1; w < tpc / 32; ++w) {
-        s1 += red[w0 + w][0];
-        s2 += red[w0 + w][1];
-      }
-    }
-  }
-  if (lane == 0 && c < C) {
+  if (owner) {
     if (a.bwd) {  // this replica's own sums (weight / bias gradients)
       if (a.out2[rep]) a.out2[rep][c] = (float)s1;
       if (a.out3[rep]) a.out3[rep][c] = (float)s2;
@@ -435,7 +398,7 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
   // one rank, one replica: every thread reads back only its own records -- no barrier
   const bool sync = a.world > 1;
   if (sync && !bn_barrier(a, rank, nblk, seen + 1u)) return;
-  if (lane == 0 && c < C) {
+  if (owner) {
     // every rank's record is requested before any is added (one NVLink round trip,
     // not world of them), then folded in ascending rank order
     double r0[RP_MAX_RANKS], r1[RP_MAX_RANKS], r2[RP_MAX_RANKS];
@@ -473,6 +436,159 @@ __device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk
   // advance the call count (after this block's barrier every block of this rank has
   // read `seen`; the state is local). One rank: the count still flips the parity.
   if (blk == 0 && threadIdx.x == 0) state_store(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE, seen + 1u);
+}
+
+__device__ __forceinline__ void exchange_body(const ExArgs& a, int rank, int blk, int nblk) {
+  __shared__ double red[kExThreads][2];
+  // BN calls completed so far (one barrier each, equal on every rank); the record
+  // set alternates with its parity, so the next call can write its records while a
+  // slow peer may still be reading this one's: a rank reuses a set only after the
+  // following call's barrier, which every peer reaches after its reads
+  const uint32_t seen = state_load(a.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE);
+  const int rep = a.rank >= 0 ? 0 : rank;  // local replica index
+  const int tpc = kExThreads / a.cpb;      // threads per channel
+  const int lane = threadIdx.x % tpc;
+  const int64_t c = (int64_t)blk * a.cpb + threadIdx.x / tpc;
+  const int64_t C = a.C;
+  // fold the S split partials of channel c: thread `lane` of the channel's tpc
+  // threads sums splits lane, lane + tpc, ...; the tpc sums are then combined by a
+  // fixed shuffle tree (warp) and a fixed-order pass over warp sums -- deterministic,
+  // and log-depth (a serial pass over 256 values cost ~4 us at C = 128)
+  double s1 = 0.0, s2 = 0.0;
+  if (c < C) {
+    const double* P = a.part[rep];
+#pragma unroll 4
+    for (int s = lane; s < a.S; s += tpc) {
+      s1 += P[((int64_t)s * C + c) * 2];
+      s2 += P[((int64_t)s * C + c) * 2 + 1];
+    }
+  }
+  const int width = tpc < 32 ? tpc : 32;
+  for (int o = width >> 1; o > 0; o >>= 1) {
+    s1 += __shfl_down_sync(0xffffffffu, s1, o, width);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o, width);
+  }
+  if (tpc > 32) {  // one partial per warp, folded in warp order by the channel's first thread
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x >> 5][0] = s1;
+      red[threadIdx.x >> 5][1] = s2;
+    }
+    __syncthreads();
+    if (lane == 0) {
+      const int w0 = threadIdx.x >> 5;
+      for (int w = 1; w < tpc / 32; ++w) {
+        s1 += red[w0 + w][0];
+        s2 += red[w0 + w][1];
+      }
+    }
+  }
+  finish_exchange(a, rank, blk, nblk, seen, c, lane == 0 && c < C, s1, s2);
+}
+
+// --- K5s: small layers (NHWC) in ONE pass with no split partials ---------------
+// Block b owns channel-vectors [b*cvb, (b+1)*cvb) over ALL rows: thread t takes
+// channel-vector t % cvb and rows t / cvb + k*RY (RY = 256 / cvb), sums them (f32
+// chunks of U rows into f64, as nhwc_partial), the RY row groups are folded by a
+// fixed shared-memory tree, and the block publishes its channels' records and meets
+// its peers directly (finish_exchange). No split partials in global memory, no
+// device-wide barrier, no separate exchange blocks: a small layer (a 4 MiB SN-GAN
+// layer took 16.4 us at one rank, 25.6 us at two, against 8.1 us for the apply on
+// the same tensor) is then one short pass plus one rank-level meeting.
+struct BnSmallArgs {
+  const void* x[RP_MAX_RANKS];
+  const void* dy[RP_MAX_RANKS];
+  const float* mean[RP_MAX_RANKS];
+  int64_t rows, C;
+  int cvb;  // channel-vectors per block (power of two)
+};
+
+template <typename T, bool BWD, int NV>
+__global__ void __launch_bounds__(kBnThreads) bn_stats_small(const ExArgs e, const BnSmallArgs b) {
+  extern __shared__ double sm[];  // [RY][cvb][NV][2]
+  const int rank = e.rank >= 0 ? e.rank : (int)blockIdx.y;
+  if (rp_aborted(e.t, rank)) return;
+  const int rep = e.rank >= 0 ? 0 : rank;
+  const int cvb = b.cvb, RY = kBnThreads / cvb;
+  const int t = threadIdx.x, cv = t % cvb, ry = t / cvb;
+  const int64_t C = b.C, M = b.rows;
+  const int64_t c0 = ((int64_t)blockIdx.x * cvb + cv) * NV;
+  const bool active = c0 < C;
+  const T* x = (const T*)b.x[rep];
+  const T* dy = BWD ? (const T*)b.dy[rep] : nullptr;
+  const uint32_t seen = state_load(e.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE);
+  double s1[NV], s2[NV];
+  float muf[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    s1[k] = s2[k] = 0.0;
+    muf[k] = (BWD && active) ? b.mean[rep][c0 + k] : 0.0f;
+  }
+  if (active) {
+    constexpr int U = 4;
+    for (int64_t r = ry; r < M; r += (int64_t)RY * U) {
+      uint4 px[U], pd[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t rr = r + (int64_t)u * RY;
+        if (rr < M) {
+          px[u] = ld128_stream(x + rr * C + c0);
+          if (BWD) pd[u] = ld128_stream(dy + rr * C + c0);
+        }
+      }
+      float f1[NV], f2[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) f1[k] = f2[k] = 0.0f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r + (int64_t)u * RY < M) {
+          Pack16<T> vx, vd;
+          vx.u = px[u];
+          if (BWD) vd.u = pd[u];
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            const float xk = to_acc(vx.e[k]);
+            if (BWD) {
+              const float dk = to_acc(vd.e[k]);
+              f1[k] += dk;
+              f2[k] = fmaf(dk, xk - muf[k], f2[k]);
+            } else {
+              f1[k] += xk;
+              f2[k] = fmaf(xk, xk, f2[k]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        s1[k] += (double)f1[k];
+        s2[k] += (double)f2[k];
+      }
+    }
+  }
+  // fixed-order tree over the RY row groups (RY is a power of two)
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    sm[(((size_t)ry * cvb + cv) * NV + k) * 2] = s1[k];
+    sm[(((size_t)ry * cvb + cv) * NV + k) * 2 + 1] = s2[k];
+  }
+  __syncthreads();
+  for (int h = RY >> 1; h > 0; h >>= 1) {
+    if (ry < h) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const size_t i = (((size_t)ry * cvb + cv) * NV + k) * 2, j = (((size_t)(ry + h) * cvb + cv) * NV + k) * 2;
+        sm[i] += sm[j];
+        sm[i + 1] += sm[j + 1];
+      }
+    }
+    __syncthreads();
+  }
+  // one thread per channel of this block publishes and folds
+  const int j = threadIdx.x;  // channel j of the block's cvb * NV
+  const int64_t c = (int64_t)blockIdx.x * cvb * NV + j;
+  const bool owner = j < cvb * NV && c < C;
+  const double v1 = owner ? sm[(size_t)j * 2] : 0.0, v2 = owner ? sm[(size_t)j * 2 + 1] : 0.0;
+  finish_exchange(e, rank, blockIdx.x, gridDim.x, seen, c, owner, v1, v2);
 }
 
 __global__ void __launch_bounds__(kExThreads) bn_exchange(const ExArgs a) {
@@ -733,6 +849,49 @@ const void* pick_fused(int dtype, bool vec) {
   return nullptr;
 }
 
+// The exchange arguments of one statistics call (outputs, records, counts).
+void fill_ex(rp_comm* c, bool bwd, float eps, int64_t rows, int64_t hw, int64_t ch, float* o0, float* o1, float* o2,
+             float* o3, double* count, ExArgs& e) {
+  const int W = c->world;
+  const int nrep = c->is_virtual ? W : 1;
+  memset(&e, 0, sizeof(e));
+  e.t = c->table;
+  e.bn_off = c->bn_records();
+  e.C = ch;
+  e.world = W;
+  e.rank = c->is_virtual ? -1 : c->rank;
+  e.bwd = bwd ? 1 : 0;
+  e.eps = eps;
+  e.timeout_ns = c->timeout_ns;
+  for (int i = 0; i < nrep; ++i) {
+    e.local_count[i] = (double)rows * (double)hw;
+    if (c->is_virtual) {
+      e.out0[i] = ((float* const*)o0)[i];
+      e.out1[i] = ((float* const*)o1)[i];
+      e.out2[i] = o2 ? ((float* const*)o2)[i] : nullptr;
+      e.out3[i] = o3 ? ((float* const*)o3)[i] : nullptr;
+      e.count[i] = count ? ((double* const*)count)[i] : nullptr;
+    } else {
+      e.out0[i] = o0;
+      e.out1[i] = o1;
+      e.out2[i] = o2;
+      e.out3[i] = o3;
+      e.count[i] = count;
+    }
+  }
+}
+
+const void* small_kernel(bool bwd, int dtype) {
+#define RP_S(DT, T)                                                                        \
+  if (dtype == DT) return bwd ? (const void*)bn_stats_small<T, true, 16 / sizeof(T)>       \
+                              : (const void*)bn_stats_small<T, false, 16 / sizeof(T)>;
+  RP_S(RP_F32, float)
+  RP_S(RP_BF16, __nv_bfloat16)
+  RP_S(RP_F16, __half)
+#undef RP_S
+  return nullptr;  // f64: the split path
+}
+
 int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, int64_t rows, int64_t ch, int64_t hw,
               int layout, float eps, const float* mean, float* o0, float* o1, float* o2, float* o3, double* count,
               cudaStream_t stream) {
@@ -766,6 +925,38 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
     if (bwd) {
       a.dy[i] = c->is_virtual ? ((const void* const*)dy)[i] : dy;
       a.mean[i] = c->is_virtual ? ((const float* const*)mean)[i] : mean;
+    }
+  }
+  // K5s: small NHWC layers in one pass (bn_stats_small); RP_BN_SMALL=0 disables (A/B)
+  {
+    const char* se = getenv("RP_BN_SMALL");
+    const void* sf = small_kernel(bwd, dtype);
+    if (layout == RP_LAYOUT_NHWC && vecok && sf && rows > 0 && !(se && se[0] == '0')) {
+      const int64_t CVt = ch / nv;
+      int cvb = 1;  // >= 128 blocks when C allows, at most 16 channel-vectors per block
+      while (cvb < 16 && CVt / (cvb * 2) >= 128) cvb *= 2;
+      const int RY = kBnThreads / cvb;
+      const int64_t blocks = (CVt + cvb - 1) / cvb;
+      const size_t ssm = (size_t)kBnThreads * nv * 2 * sizeof(double);
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sf, kBnThreads, ssm) != cudaSuccess || occ < 1) occ = 1;
+      const int64_t wave = rp_wave_per_rank(c, occ);
+      if (rows <= (int64_t)32 * RY && blocks <= wave) {
+        BnSmallArgs b;
+        memset(&b, 0, sizeof(b));
+        for (int i = 0; i < nrep; ++i) {
+          b.x[i] = a.x[i];
+          b.dy[i] = a.dy[i];
+          b.mean[i] = a.mean[i];
+        }
+        b.rows = rows;
+        b.C = ch;
+        b.cvb = cvb;
+        ExArgs e;
+        fill_ex(c, bwd, eps, rows, hw, ch, o0, o1, o2, o3, count, e);
+        void* args[] = {&e, &b};
+        return rp_launch(c, sf, dim3((unsigned)blocks, nrep), dim3(kBnThreads), args, ssm, stream);
+      }
     }
   }
   dim3 grid, block;
@@ -839,33 +1030,9 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
   }
 
   ExArgs e;
-  memset(&e, 0, sizeof(e));
-  e.t = c->table;
-  e.bn_off = c->bn_records();
-  e.C = ch;
+  fill_ex(c, bwd, eps, rows, hw, ch, o0, o1, o2, o3, count, e);
   e.S = a.S;
-  e.world = W;
-  e.rank = c->is_virtual ? -1 : c->rank;
-  e.bwd = bwd ? 1 : 0;
-  e.eps = eps;
-  e.timeout_ns = c->timeout_ns;
-  for (int i = 0; i < nrep; ++i) {
-    e.part[i] = a.part[i];
-    e.local_count[i] = (double)rows * (double)hw;
-    if (c->is_virtual) {
-      e.out0[i] = ((float* const*)o0)[i];
-      e.out1[i] = ((float* const*)o1)[i];
-      e.out2[i] = o2 ? ((float* const*)o2)[i] : nullptr;
-      e.out3[i] = o3 ? ((float* const*)o3)[i] : nullptr;
-      e.count[i] = count ? ((double* const*)count)[i] : nullptr;
-    } else {
-      e.out0[i] = o0;
-      e.out1[i] = o1;
-      e.out2[i] = o2;
-      e.out3[i] = o3;
-      e.count[i] = count;
-    }
-  }
+  for (int i = 0; i < nrep; ++i) e.part[i] = a.part[i];
   if (fused) {  // one launch: partials, device-wide barrier, exchange (bn_stats_fused)
     e.cpb = fcpb;
     FusedBnArgs fa;

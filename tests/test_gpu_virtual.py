@@ -352,8 +352,14 @@ def _bn_virtual(comm, xs, layout, rows, c, hw, eps=1e-5):
 
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-@pytest.mark.parametrize("shape", [(8, 64, 16, 16), (4, 256, 4, 4), (3, 33, 5, 7), (2, 1024, 1, 1)])
-def test_bn_stats_match_f64_oracle(layout, dtype, shape):
+@pytest.mark.parametrize("shape", [(8, 64, 16, 16), (4, 256, 4, 4), (3, 33, 5, 7), (2, 1024, 1, 1),
+                                   (64, 128, 16, 16)])
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_bn_stats_match_f64_oracle(layout, dtype, shape, small, monkeypatch):
+    """Both NHWC statistics paths: the one-pass small-layer kernel (bn_stats_small,
+    the default where it applies) and the split-partials kernel (RP_BN_SMALL=0, and
+    the 64x128x16x16 layer, too many rows for the one-pass form)."""
+    monkeypatch.setenv("RP_BN_SMALL", small)
     n = 4
     comm = vcomm(n)
     g = torch.Generator(device=DEV).manual_seed(7)
@@ -374,7 +380,10 @@ def test_bn_stats_match_f64_oracle(layout, dtype, shape):
         assert host(mean[r]).tobytes() == host(mean[0]).tobytes()  # symmetric
 
 
-def test_bn_bwd_stats_match_oracle():
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_bn_bwd_stats_match_oracle(layout, small, monkeypatch):
+    monkeypatch.setenv("RP_BN_SMALL", small)
     n, shape = 2, (4, 32, 6, 6)
     comm = vcomm(n)
     lib = _lib.load()
@@ -384,10 +393,16 @@ def test_bn_bwd_stats_match_oracle():
     m_ref, *_ = O.bn_stats_per_channel([host(x) for x in xs], layout="nchw")
     mean = [to_dev(m_ref.astype(np.float32)) for _ in range(n)]
     outs = [[torch.empty(shape[1], device=DEV) for _ in range(n)] for _ in range(4)]
-    arrs = [_lib.ptr_array([t.data_ptr() for t in lst]) for lst in ([*xs], [*dys], mean, *outs)]
+    if layout == "nhwc":
+        xk = [x.permute(0, 2, 3, 1).contiguous() for x in xs]
+        dk = [d.permute(0, 2, 3, 1).contiguous() for d in dys]
+        rows_k, hw_k, lay = shape[0] * shape[2] * shape[3], 1, _lib.NHWC
+    else:
+        xk, dk, rows_k, hw_k, lay = xs, dys, shape[0], shape[2] * shape[3], _lib.NCHW
+    arrs = [_lib.ptr_array([t.data_ptr() for t in lst]) for lst in ([*xk], [*dk], mean, *outs)]
     p = [ctypes.cast(a[0], ctypes.c_void_p).value for a in arrs]
-    _lib.check(lib.rp_bn_bwd_stats(comm._handle, p[0], p[1], 0, shape[0], shape[1], shape[2] * shape[3],
-                                   _lib.NCHW, p[2], p[3], p[4], p[5], p[6],
+    _lib.check(lib.rp_bn_bwd_stats(comm._handle, p[0], p[1], 0, rows_k, shape[1], hw_k,
+                                   lay, p[2], p[3], p[4], p[5], p[6],
                                    torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     rows = [O._channel_view(host(x), "nchw") for x in xs]
