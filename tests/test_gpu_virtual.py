@@ -181,7 +181,7 @@ def test_bf16_all_reduce_matches_oracle(n, impl):
     xs = [to_dev(b.view(np.int16)).view(torch.bfloat16) for b in bits]
     for kind in ("sum", "mean", "premean", "max"):
         want = O.fold_bf16(bits, kind)
-        for algo in ("oneshot", "twoshot"):
+        for algo in ("oneshot", "twoshot", "flat"):
             outs = vcomm(n).all_reduce(xs, kind, algo=algo)
             for o in outs:
                 got = host(o.view(torch.int16)).view(np.uint16)
@@ -193,7 +193,7 @@ def test_f32_grads_exchanged_as_bf16(impl):
     rng = np.random.default_rng(31)
     xs_np = [rng.standard_normal(30011).astype(np.float32) for _ in range(n)]
     want = O.bf16_bits_to_f32(O.fold_bf16([O.f32_to_bf16_bits(x) for x in xs_np], "premean"))
-    for algo in ("oneshot", "twoshot"):
+    for algo in ("oneshot", "twoshot", "flat"):  # flat: the cast fused on load and on store
         outs = vcomm(n).all_reduce([to_dev(x) for x in xs_np], "premean", comm_dtype=torch.bfloat16, algo=algo)
         for o in outs:
             assert o.dtype == torch.float32
