@@ -708,7 +708,7 @@ const void* pick_ar(int algo, int world, int push) {
                                      : (const void*)ar_twoshot_dyn<DT, OP, NR, true>;           \
     return algo == RP_ALGO_ONESHOT ? (const void*)ar_oneshot<DT, OP, NR>                        \
                                    : (const void*)ar_twoshot_dyn<DT, OP, NR, false>;
-  if (algo == RP_ALGO_FLAT + 100) {  // bulk-copy form of the flat kernel
+  if (algo == RP_ALGO_FLAT_BULK) {  // bulk-copy form of the flat kernel (internal selector)
     switch (world) {
       case 2: return (const void*)ar_virtual_flat_bulk<DT, OP, 2>;
       case 3: return (const void*)ar_virtual_flat_bulk<DT, OP, 3>;

@@ -459,7 +459,7 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
       bool ok = be[0] == '1' && dtype_in == dtype_comm && dtype_out == dtype_comm;
       for (int i = 0; i < W && ok; ++i) ok = ((((uintptr_t)src[i]) | ((uintptr_t)dst[i])) & 15u) == 0;
       if (ok) {
-        const void* fb = pick_ar_any(dtype_comm, op, RP_ALGO_FLAT + 100, W, 0);
+        const void* fb = pick_ar_any(dtype_comm, op, RP_ALGO_FLAT_BULK, W, 0);
         if (!fb) return rp_fail(RP_ERR_INVALID, "all_reduce(flat bulk): unsupported replica count (2..8)");
         const size_t smem = rp_bulk_smem_bytes(W);
         RP_CUDA_CHECK(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -11,6 +11,8 @@
 #include "../../include/rp.h"
 
 #define RP_MAX_RANKS 8
+// internal kernel selector (not an ABI algorithm): the bulk-copy form of RP_ALGO_FLAT
+#define RP_ALGO_FLAT_BULK 105
 // Signal slots: one row of RP_MAX_RANKS u32 per block index. Rows
 // [0, RP_MAX_BLOCKS) carry the per-block barriers of the collectives; rows
 // [RP_BN_ROW0, RP_BN_ROW0 + RP_BN_ROWS) those of the BN statistics exchange.
