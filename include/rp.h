@@ -253,12 +253,31 @@ RP_API int rp_all_reduce_algo(rp_comm_t comm, const void* src, const void* dst, 
 /* The plan rp_all_reduce would follow, for cross-rank agreement checks
  * (Replicator(check_protocol=True) digests it): plan[0] = algorithm (AUTO
  * resolved), plan[1] = 1 for the push data-movement form, plan[2] / plan[3] = pool
- * offset of src / dst, or -1 when outside the pool. Ranks MUST agree on all four
+ * offset of src / dst, -2 for a registered user buffer (rp_register_*), -1 for
+ * any other buffer. Ranks MUST agree on all four
  * (symmetric placement): a rank passing a pool view where a peer passes a plain
  * tensor would launch a different kernel against the shared barrier state.
  * Multi-process communicators only look at this rank's pointers. */
 RP_API int rp_all_reduce_plan(rp_comm_t comm, const void* src, const void* dst, size_t count, int dtype_in,
                               int dtype_comm, int dtype_out, int op, int algo, int64_t* plan);
+
+/* ---- user-buffer registration -------------------------------------------
+ * Collective: every rank registers its corresponding buffer (same size, same
+ * order). rp_register_export fills this rank's blob (the buffer's allocation
+ * exported with cudaIpcGetMemHandle, plus its offset; a loopback world: the plain
+ * pointer); the caller exchanges the blobs (rank order) and passes them all to
+ * rp_register_import, which maps every peer's copy (each peer allocation opened
+ * once, refcounted) and returns the registration index. Afterwards an in-place
+ * rp_all_reduce of the buffer (or of a sub-range at the same offset on every rank),
+ * without a cast, takes the zero-copy pull two-shot -- the path pool buckets take
+ * -- instead of the push form with staging (rp_all_reduce_plan reports -2 as its
+ * placement). Stream-ordered-pool and expandable-segment memory cannot be shared
+ * over CUDA IPC (RP_ERR_CONFIG). The caller keeps the buffers alive until
+ * rp_unregister (collective) or rp_comm_destroy. */
+RP_API size_t rp_register_export_size(void);
+RP_API int rp_register_export(rp_comm_t comm, const void* ptr, size_t bytes, void* blob, size_t* len);
+RP_API int rp_register_import(rp_comm_t comm, const void* all, size_t len, int* reg);
+RP_API int rp_unregister(rp_comm_t comm, int reg);
 
 /* dst[r*bytes_per_rank ...] = src of rank r (rank order, graph.py:575-579). */
 RP_API int rp_all_gather(rp_comm_t comm, const void* src, void* dst, size_t bytes_per_rank, void* stream);

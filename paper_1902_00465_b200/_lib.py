@@ -75,6 +75,10 @@ SIGNATURES = {
     "rp_comm_set_timeout": (_i, [_c_void_p, ctypes.c_uint64]),
     "rp_comm_set_block_cap": (_i, [_c_void_p, ctypes.c_int]),
     "rp_all_reduce": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _i, _i, _i, _c_void_p]),
+    "rp_register_export_size": (_size_t, []),
+    "rp_register_export": (_i, [_c_void_p, _c_void_p, _size_t, _c_void_p, ctypes.POINTER(_size_t)]),
+    "rp_register_import": (_i, [_c_void_p, _c_void_p, _size_t, ctypes.POINTER(_i)]),
+    "rp_unregister": (_i, [_c_void_p, _i]),
     "rp_all_gather": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _c_void_p]),
     "rp_broadcast": (_i, [_c_void_p, _c_void_p, _c_void_p, _size_t, _i, _i, _c_void_p]),
     "rp_apply_shard": (_i, [_c_void_p, _size_t, _i, ctypes.POINTER(_size_t), ctypes.POINTER(_size_t)]),

@@ -371,6 +371,31 @@ class Communicator(_Base):
         off = self._reserve(numel * esz)
         return tensor_at(self._pool_ptr(self.rank) + off, numel, dtype, self.device, self)
 
+    # -- user-buffer registration (include/rp.h rp_register_*) -----------------
+    def register(self, t: torch.Tensor) -> "Registration":
+        """Collective (every rank, same order, same size): map this rank's ``t`` on
+        every peer once, so that in-place all-reduces of ``t`` -- or of a view at the
+        same offset inside it on every rank -- run the zero-copy pull two-shot like
+        pool buckets (no staging). Keep ``t`` alive until ``unregister``. Needs
+        IPC-shareable memory (PyTorch's default caching allocator; a loopback world
+        shares plain pointers)."""
+        if not t.is_cuda or t.device.index != self.device or not _is_dense(t):
+            raise errors.ShapeError("register: a dense CUDA tensor on this communicator's device")
+        size = self._lib.rp_register_export_size()
+        buf = ctypes.create_string_buffer(size)
+        n = ctypes.c_size_t(size)
+        _lib.check(self._lib.rp_register_export(self._handle, t.data_ptr(), t.numel() * t.element_size(), buf,
+                                                ctypes.byref(n)), "register")
+        joined = exchange_blobs(bytes(buf.raw[: n.value]), self.bootstrap) if self.world > 1 else bytes(buf.raw[: n.value])
+        reg = ctypes.c_int(-1)
+        _lib.check(self._lib.rp_register_import(self._handle, joined, len(joined), ctypes.byref(reg)), "register")
+        return Registration(self, reg.value, t)
+
+    def unregister(self, reg: "Registration") -> None:
+        """Collective: release a registration (peers' mappings closed when unused)."""
+        _lib.check(self._lib.rp_unregister(self._handle, reg.index), "unregister")
+        reg.index = -1
+
     # -- NVLS (NVLink SHARP) region -------------------------------------------
     def enable_nvls(self, nbytes: int, group=None) -> None:
         """Bind ``nbytes`` of this rank's memory to one multicast object spanning all
@@ -562,6 +587,17 @@ class Communicator(_Base):
             other = bytes(d[bad[0]].numpy()).rstrip(b"\0").decode(errors="replace")
             raise errors.ProtocolError(f"collective protocol mismatch: rank {self.rank} issued {desc}, "
                                        f"rank {bad[0]} issued {other} (ranks {bad} disagree with rank {self.rank})")
+
+
+class Registration:
+    """A buffer registered with every peer (Communicator.register); keeps the tensor
+    alive while registered."""
+
+    def __init__(self, comm, index: int, tensor: torch.Tensor):
+        self.comm, self.index, self.tensor = comm, index, tensor
+
+    def __repr__(self):
+        return f"Registration(index={self.index}, numel={self.tensor.numel()}, dtype={self.tensor.dtype})"
 
 
 class VirtualCommunicator(_Base):

@@ -337,6 +337,15 @@ void base_args(rp_comm* c, CollArgs& a) {
   a.timeout_ns = c->timeout_ns;
 }
 
+// An in-place all-reduce of a registered user buffer (rp_register_*), no cast:
+// every peer's copy is addressable, so the zero-copy pull two-shot applies.
+bool registered_in_place(rp_comm* c, const void* const* src, const void* const* dst, size_t count, int dtype_in,
+                         int dtype_comm, int dtype_out, int* reg, size_t* off) {
+  if (c->is_virtual || c->regs.empty() || src[0] != dst[0] || dtype_in != dtype_comm || dtype_out != dtype_comm)
+    return false;
+  return rp_registered(c, src[0], count * rp_dtype_size(dtype_comm), reg, off);
+}
+
 }  // namespace
 
 // shared with rp_apply.cu (fused optimizer apply)
@@ -393,13 +402,17 @@ void rp_plan_all_reduce(rp_comm* c, const void* const* src, const void* const* d
   size_t so = 0, doff = 0;
   const bool sp = symmetric_in_pool(c, src, count * rp_dtype_size(dtype_in), &so);
   const bool dp = symmetric_in_pool(c, dst, count * rp_dtype_size(dtype_out), &doff);
+  int reg = -1;
+  size_t roff = 0;
+  const bool rg = registered_in_place(c, src, dst, count, dtype_in, dtype_comm, dtype_out, &reg, &roff);
   int push = 0;
-  if (!c->is_virtual && a != RP_ALGO_NVLS) push = (a == RP_ALGO_ONESHOT || !(sp && dtype_in == dtype_comm)) ? 1 : 0;
+  if (!c->is_virtual && a != RP_ALGO_NVLS)
+    push = (a == RP_ALGO_ONESHOT || !((sp || rg) && dtype_in == dtype_comm)) ? 1 : 0;
   if (const char* e = getenv("RP_AR_IMPL")) push = (e[0] == 'p' && e[1] == 'u' && e[2] == 's') ? 1 : 0;
   plan[0] = a;
   plan[1] = push;
-  plan[2] = sp ? (int64_t)so : -1;
-  plan[3] = dp ? (int64_t)doff : -1;
+  plan[2] = sp ? (int64_t)so : (rg ? -2 : -1);
+  plan[3] = dp ? (int64_t)doff : (rg ? -2 : -1);
 }
 
 int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, size_t count,
@@ -507,10 +520,31 @@ int rp_launch_all_reduce(rp_comm* c, const void* const* src, void* const* dst, s
     push = 1;
   } else {
     size_t off0;
-    push = (dtype_in == dtype_comm && symmetric_in_pool(c, src, count * rp_dtype_size(dtype_in), &off0)) ? 0 : 1;
+    int reg0;
+    push = (dtype_in == dtype_comm &&
+            (symmetric_in_pool(c, src, count * rp_dtype_size(dtype_in), &off0) ||
+             registered_in_place(c, src, (const void* const*)dst, count, dtype_in, dtype_comm, dtype_out, &reg0, &off0)))
+               ? 0 : 1;
   }
   if (const char* e = getenv("RP_AR_IMPL")) push = (e[0] == 'p' && e[1] == 'u' && e[2] == 's') ? 1 : 0;
   if (push) return launch_push(c, src, dst, count, dtype_in, dtype_comm, dtype_out, op, algo, stream, a);
+
+  // a registered user buffer, in place: the pool two-shot with every rank's copy
+  // of the buffer as the data table (read_off = write_off = the offset inside it)
+  {
+    int reg = -1;
+    size_t roff = 0;
+    if (algo == RP_ALGO_TWOSHOT &&
+        registered_in_place(c, src, (const void* const*)dst, count, dtype_in, dtype_comm, dtype_out, &reg, &roff)) {
+      const void* fn = pick_ar_any(dtype_comm, op, RP_ALGO_TWOSHOT, W, 0);
+      if (!fn) return rp_fail(RP_ERR_INVALID, "all_reduce: unsupported world size (1..8)");
+      for (int p = 0; p < W; ++p) a.t.data[p] = c->regs[reg].ptr[p];
+      a.read_off = a.write_off = roff;
+      a.copy_in = a.copy_out = 0;
+      a.chunk = (V + W - 1) / W;
+      return dyn_launch(c, fn, a, stream, "twoshot_registered", 0, kThreads, 0);
+    }
+  }
 
   // Placement. Pool-resident buffers (symmetric offsets, allocated identically on
   // every rank) are exchanged zero-copy; anything else is staged through scratch.

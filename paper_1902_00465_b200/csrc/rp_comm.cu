@@ -578,6 +578,7 @@ int rp_comm_destroy(rp_comm_t c) {
   if (!c) return RP_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  rp_release_registrations(c);
   rp_nvls_destroy(c);
   if (c->lb_refs) {
     // every rank's region, freed by whichever rank lets go of it last

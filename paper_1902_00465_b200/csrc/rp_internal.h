@@ -5,6 +5,7 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -79,6 +80,15 @@ struct RankTable {
   uint32_t* sig[RP_MAX_RANKS];    // signal region base of every rank (peer-mapped)
 };
 
+// A user buffer registered with every peer (rp_register_*): the base pointer of
+// the same buffer on every rank (IPC-mapped, or loopback plain pointers).
+struct RpReg {
+  char* ptr[RP_MAX_RANKS] = {};
+  size_t bytes = 0;
+  bool live = false;
+  std::string ipc_key[RP_MAX_RANKS];  // opened IPC handle per peer ("" = not IPC)
+};
+
 struct rp_comm {
   int rank = 0;
   int world = 1;
@@ -101,6 +111,9 @@ struct rp_comm {
   bool loopback = false;
   int loopback_cap = 0;    // num_sms / world in a loopback world
   bool lb_refs = false;    // holds a reference on every rank's region (loopback registry)
+  // registered user buffers and the peer IPC mappings they hold (refcounted by handle)
+  std::vector<RpReg> regs;
+  std::map<std::string, std::pair<char*, int>> ipc_cache;
   // topology discovered by rp_comm_import (rp_comm_topology)
   int links[RP_MAX_RANKS] = {};
   int nvlinks[RP_MAX_RANKS] = {};
@@ -162,6 +175,10 @@ struct CollArgs {
 };
 
 int rp_classify_link(rp_comm* c, const RpExport& me, const RpExport& peer, bool self, std::string* why);
+
+// [p, p + bytes) lies inside one live registration: its index and the offset
+bool rp_registered(rp_comm* c, const void* p, size_t bytes, int* reg, size_t* off);
+void rp_release_registrations(rp_comm* c);
 
 // error plumbing
 void rp_set_error(const std::string& msg);

@@ -352,6 +352,47 @@ def body_random_sequence(rank, world, env):
     comm.close()
 
 
+def body_register(rank, world, env):
+    """User-buffer registration (include/rp.h rp_register_*): in-place all-reduces of
+    a registered tensor, and of a view at the same offset inside it, take the
+    zero-copy pull two-shot (plan placement -2) and equal the oracle fold bit for
+    bit, back to back; small messages keep the push one-shot; after unregister the
+    buffer is a plain user buffer again (push form, placement -1)."""
+    from oracle import collectives as O
+    from paper_1902_00465_b200.comm import Communicator
+
+    dev = env.dev
+    comm = Communicator(device=env.device, bootstrap=env.bootstrap, pool_bytes=32 << 20)
+    count = 3 << 20
+    x = torch.empty(count, device=dev)
+    reg = comm.register(x)
+    assert comm.plan_for(x, "sum", out=x) == (2, 0, -2, -2), comm.plan_for(x, "sum", out=x)
+    for it in range(3):
+        xs = _inputs(world, count, seed=4000 + it)
+        x.copy_(torch.from_numpy(xs[rank]))
+        comm.all_reduce_tensor(x, "premean", out=x)
+        assert H(x).numpy().tobytes() == O.fold_premean(xs).tobytes(), it
+    xs = _inputs(world, count, seed=4100)
+    x.copy_(torch.from_numpy(xs[rank]))
+    v = x[4096:4096 + (1 << 20)]
+    comm.all_reduce_tensor(v, "sum", out=v)
+    want = O.fold_sum([a[4096:4096 + (1 << 20)] for a in xs])
+    assert H(v).numpy().tobytes() == want.tobytes()
+    assert H(x[:4096]).numpy().tobytes() == xs[rank][:4096].tobytes()  # nothing outside the view
+    small = x[:1000]
+    assert comm.plan_for(small, "sum", out=small)[:2] == (1, 1)  # one-shot, push
+    comm.all_reduce_tensor(small, "max", out=small)
+    assert H(small).numpy().tobytes() == O.fold_max([a[:1000] for a in xs]).tobytes()
+    comm.unregister(reg)
+    assert comm.plan_for(x, "sum", out=x) == (2, 1, -1, -1)
+    xs = _inputs(world, count, seed=4200)
+    x.copy_(torch.from_numpy(xs[rank]))
+    comm.all_reduce_tensor(x, "sum", out=x)
+    assert H(x).numpy().tobytes() == O.fold_sum(xs).tobytes()
+    comm.check()
+    comm.close()
+
+
 def body_bn(rank, world, env):
     from oracle import collectives as O
     from paper_1902_00465_b200.replicator import CrossReplicaBatchNorm, Replicator

@@ -118,6 +118,12 @@ def test_back_to_back_random_sequence_loopback(world):
 
 
 @pytest.mark.timeout(300)
+@W248
+def test_registered_user_buffers_loopback(world):
+    run_loopback("body_register", world)
+
+
+@pytest.mark.timeout(300)
 def test_reference_mesh_seam_replay_loopback():
     run_loopback("body_mesh_seam", 2)
 

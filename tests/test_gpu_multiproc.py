@@ -85,6 +85,10 @@ def test_back_to_back_random_sequence_multiprocess():
     run_world("body_random_sequence")
 
 
+def test_registered_user_buffers_multiprocess():
+    run_world("body_register")
+
+
 def test_cross_replica_bn_autograd_multiprocess():
     run_world("body_bn")
 
