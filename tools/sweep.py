@@ -57,6 +57,10 @@ def main():
     bufs = [torch.randn(count_max, device=dev) for _ in range(reps)]
     outs = [torch.empty(n * count_max if "all_gather" in a.ops else count_max, device=dev) for _ in range(reps)]
     nvls_buf = None
+    reg_buf = None
+    if "registered" in a.algos.split(",") and world > 1:  # a registered user tensor, reduced in place (zero-copy)
+        reg_buf = torch.randn(count_max, device=dev)
+        comm.register(reg_buf)
     if "nvls" in a.algos.split(",") and world > 1:  # in-switch reduction: in place in the multicast region
         comm.enable_nvls(maxb + (4 << 20))
         nvls_buf = comm.alloc_nvls(count_max, torch.float32)
@@ -99,6 +103,10 @@ def main():
                             continue
                         fn = lambda: comm.all_reduce_tensor(nvls_buf[:count], "mean", out=nvls_buf[:count],  # noqa: E731
                                                             algo="nvls")
+                    elif algo == "registered":
+                        if reg_buf is None:
+                            continue
+                        fn = lambda: comm.all_reduce_tensor(reg_buf[:count], "mean", out=reg_buf[:count])  # noqa: E731
                     else:
                         fn = lambda: comm.all_reduce_tensor(xs[0], "sum", out=os_[0], algo=algo)  # noqa: E731
                     factor = 2.0 * (n - 1) / n
