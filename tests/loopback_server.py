@@ -1,4 +1,4 @@
-"""Child process serving the loopback-world tests (test_gpu_loopback.py).
+"""Child process serving the loopback-world tests (test_gpu_world_loopback.py).
 
 A loopback world needs PyTorch's stream-ordered allocator (bootstrap.py
 LoopbackWorld), which must be chosen before CUDA initialises; running the worlds in

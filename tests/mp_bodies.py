@@ -2,7 +2,7 @@
 
 * ``test_gpu_multiproc.py`` -- one process per GPU over torch.distributed (gloo,
   handle exchange only): the NVLink path proper (needs >= 2 GPUs);
-* ``test_gpu_loopback.py`` -- a LoopbackWorld (bootstrap.py): W ranks in one
+* ``test_gpu_world_loopback.py`` -- a LoopbackWorld (bootstrap.py): W ranks in one
   process on ONE GPU, one host thread and stream each, the same kernels, barriers
   and algorithm choices with local HBM in place of NVLink (runs on the driver's
   1-GPU box).

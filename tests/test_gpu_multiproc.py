@@ -2,7 +2,7 @@
 torch.distributed (gloo, handle exchange only), kernels loading/storing peer pools.
 Needs >= 2 GPUs (``gpurun --gpus 2`` / ``--gpus 4``); skipped otherwise. The rank
 bodies live in tests/mp_bodies.py and also run in a one-GPU loopback world
-(test_gpu_loopback.py)."""
+(test_gpu_world_loopback.py)."""
 
 import os
 import socket

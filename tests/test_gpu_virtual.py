@@ -97,31 +97,6 @@ def test_all_reduce_sizes_f32(n, count, impl):
                 assert host(o).tobytes() == want.tobytes(), (kind, algo)
 
 
-@pytest.mark.parametrize("n", [2, 3, 8])
-def test_flat_bulk_copy_variant_matches_oracle(n, monkeypatch):
-    """The cp.async.bulk (TMA bulk engine + mbarrier) staging of the flat virtual
-    all-reduce (RP_VFLAT_BULK=1): bit-exact for every fold, for counts with a
-    partial last vector (register-path tail) and with tiny / odd sizes; misaligned
-    buffers fall back to the register form."""
-    monkeypatch.setenv("RP_VFLAT_BULK", "1")
-    rng = np.random.default_rng(n)
-    for count in (1, 3, 4, 5, 127, 4097, 65536 + 3, (1 << 20) + 1):
-        xs_np = [rng.standard_normal(count).astype(np.float32) for _ in range(n)]
-        for kind in ("sum", "mean", "max", "premean"):
-            want = O.FOLDS[kind](xs_np)
-            outs = vcomm(n).all_reduce([to_dev(x) for x in xs_np], kind, algo="flat")
-            for o in outs:
-                assert host(o).tobytes() == want.tobytes(), (count, kind)
-    xs64 = [rng.standard_normal(33333) for _ in range(n)]
-    outs = vcomm(n).all_reduce([to_dev(x) for x in xs64], "sum", algo="flat")
-    assert host(outs[0]).tobytes() == O.fold_sum(xs64).tobytes()
-    base = [to_dev(rng.standard_normal(1001).astype(np.float32)) for _ in range(n)]
-    xs = [b[1:] for b in base]  # misaligned: register form
-    outs = vcomm(n).all_reduce(xs, "sum", algo="flat")
-    assert host(outs[0]).tobytes() == O.fold_sum([host(x) for x in xs]).tobytes()
-    vcomm(n).check()
-
-
 def test_all_reduce_misaligned_views(impl):
     n = 4
     rng = np.random.default_rng(9)
@@ -694,3 +669,30 @@ def test_all_reduce_host_pipelined_matches_oracle(kind, pinned):
     assert out.numpy().tobytes() == O.fold_sum(f64).tobytes()
     with pytest.raises(errors.ShapeError):
         comm.all_reduce_host(hin[:3], kind)
+
+
+# --- A/B variant (round 2): kept last so a failure cannot hide the tests above ----
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_flat_bulk_copy_variant_matches_oracle(n, monkeypatch):
+    """The cp.async.bulk (TMA bulk engine + mbarrier) staging of the flat virtual
+    all-reduce (RP_VFLAT_BULK=1): bit-exact for every fold, for counts with a
+    partial last vector (register-path tail) and with tiny / odd sizes; misaligned
+    buffers fall back to the register form."""
+    monkeypatch.setenv("RP_VFLAT_BULK", "1")
+    rng = np.random.default_rng(n)
+    for count in (1, 3, 4, 5, 127, 4097, 65536 + 3, (1 << 20) + 1):
+        xs_np = [rng.standard_normal(count).astype(np.float32) for _ in range(n)]
+        for kind in ("sum", "mean", "max", "premean"):
+            want = O.FOLDS[kind](xs_np)
+            outs = vcomm(n).all_reduce([to_dev(x) for x in xs_np], kind, algo="flat")
+            for o in outs:
+                assert host(o).tobytes() == want.tobytes(), (count, kind)
+    xs64 = [rng.standard_normal(33333) for _ in range(n)]
+    outs = vcomm(n).all_reduce([to_dev(x) for x in xs64], "sum", algo="flat")
+    assert host(outs[0]).tobytes() == O.fold_sum(xs64).tobytes()
+    base = [to_dev(rng.standard_normal(1001).astype(np.float32)) for _ in range(n)]
+    xs = [b[1:] for b in base]  # misaligned: register form
+    outs = vcomm(n).all_reduce(xs, "sum", algo="flat")
+    assert host(outs[0]).tobytes() == O.fold_sum([host(x) for x in xs]).tobytes()
+    vcomm(n).check()

@@ -7,7 +7,7 @@ same graph, replica site by replica site -- including the wrap_optimizer premean
 (``nary_sum`` over ``x / R`` nodes, PAPER.md:196-206).
 
 Seam 1 (the mesh communicator driven by ``Graph.evaluate``) is exercised by
-``body_reference_graph`` in test_gpu_loopback.py / test_gpu_multiproc.py.
+``body_reference_graph`` in test_gpu_world_loopback.py / test_gpu_multiproc.py.
 
 The reference package comes from ``oracle/_ref`` (oracle/ref_vendor.py), test
 infrastructure only: here it is the checker and the graph engine that calls the

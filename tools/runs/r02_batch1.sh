@@ -5,11 +5,11 @@
 set -u
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 1500 python -m pytest tests/test_gpu_loopback.py -q -p no:cacheprovider --timeout 900 --durations=15 \
+timeout 1500 python -m pytest tests/test_gpu_world_loopback.py -q -p no:cacheprovider --timeout 900 --durations=15 \
     > gpurun_out/r02_pytest_loopback.log 2>&1
 echo "loopback pytest rc=$?"; tail -3 gpurun_out/r02_pytest_loopback.log
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 --durations=10 \
-    --deselect tests/test_gpu_loopback.py > gpurun_out/r02_pytest_gpu.log 2>&1
+    --deselect tests/test_gpu_world_loopback.py > gpurun_out/r02_pytest_gpu.log 2>&1
 echo "gpu pytest rc=$?"; tail -3 gpurun_out/r02_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02_smoke.log 2>&1
 echo "smoke rc=$?"
