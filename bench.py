@@ -225,7 +225,8 @@ def _config(args, world):
                                                       else f" on {world} B200 (one per process, NVLink P2P)")),
             "msg_bytes_per_replica": args.bytes, "replicas": n, "dtype": "f32", "op": args.kind,
             "algo": getattr(args, "chosen_algo", args.algo), "algo_requested": args.algo,
-            "in_place_pool": True, "l2": ("flushed between steps (256 MiB write + 256 MiB read: clean, cold L2)"
+            "in_place_pool": True, "clock_settle": "50 ms of L2-flush traffic before the warm-up steps",
+            "l2": ("flushed between steps (256 MiB write + 256 MiB read: clean, cold L2)"
                                           if getattr(args, "flush", "write") == "write+read"
                                           else "flushed between steps (256 MiB write)"),
             "parallelism": f"dp{n}"}
@@ -289,12 +290,25 @@ def run_ours(args, rank, world, local):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    comm.check()
+    # clock sampler first (nvidia-smi needs ~0.2 s to start), so no idle gap separates
+    # the warm-up from the timed steps; then ~50 ms of flush traffic (memory only, no
+    # collective) to settle the clocks, and W warm-up steps shaped exactly like the
+    # timed ones (flush, align, step)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
+    settle_end = time.time() + 0.05
+    while time.time() < settle_end:
+        flush.zero_()
+        torch.cuda.synchronize()
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        if flush_rd is not None:
+            flush_rd.sum()
+        if align is not None:
+            align()
+        step()
+    comm.check()
     barrier()
     t_wall0 = time.time()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
