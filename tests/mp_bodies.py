@@ -783,6 +783,23 @@ def body_protocol(rank, world, env):
                for r in range(world))
     sc = repl.comm.all_gather(np.float64(rank))
     assert [float(np.asarray(v)) for v in sc] == [float(r) for r in range(world)]
+    # SPEC.md:223-231 across processes: map_gather / map_reduce deliver to the driver,
+    # readable only outside the replicated step; the list form of all_gather
+    repl.new_generation()
+
+    def step(_):
+        rows_r = torch.full((rank + 1, 2), float(rank), device=dev)
+        mg = repl.map_gather(rows_r, label="mg")
+        mr = repl.map_reduce(torch.tensor([float(rank + 1)], device=dev), "sum", label="mr")
+        with pytest.raises(errors.EvaluationError):
+            mg.value  # noqa: B018 -- reading inside the step is the SPEC's error
+        lst = repl.all_gather(torch.tensor(float(rank), device=dev), label="lst")
+        return mg, mr, lst
+    (mg, mr, lst), = repl.run(step, lambda r: None)
+    assert [tuple(t.shape) for t in mg.value] == [(r + 1, 2) for r in range(world)]
+    assert all(EQ(t, torch.full((r + 1, 2), float(r), device=dev)) for r, t in enumerate(mg.value))
+    assert float(H(mr.value)[0]) == float(sum(range(1, world + 1)))
+    assert isinstance(lst, list) and [float(H(t)) for t in lst] == [float(r) for r in range(world)]
     repl.comm.check()
     repl.comm.close()
 
