@@ -498,8 +498,8 @@ struct BnSmallArgs {
   const void* x[RP_MAX_RANKS];
   const void* dy[RP_MAX_RANKS];
   const float* mean[RP_MAX_RANKS];
-  int64_t rows, C;
-  int cvb;  // channel-vectors per block (power of two)
+  int64_t rows, C, hw;
+  int cvb;  // NHWC: channel-vectors per block; NCHW: channels per block (powers of two)
 };
 
 template <typename T, bool BWD, int NV>
@@ -588,6 +588,87 @@ __global__ void __launch_bounds__(kBnThreads) bn_stats_small(const ExArgs e, con
   const int64_t c = (int64_t)blockIdx.x * cvb * NV + j;
   const bool owner = j < cvb * NV && c < C;
   const double v1 = owner ? sm[(size_t)j * 2] : 0.0, v2 = owner ? sm[(size_t)j * 2 + 1] : 0.0;
+  finish_exchange(e, rank, blockIdx.x, gridDim.x, seen, c, owner, v1, v2);
+}
+
+// K5s for NCHW [n, C, hw]: block b owns channels [b*cpb, (b+1)*cpb), all n x hw
+// elements of each (thread t takes elements t, t+256, ... of the channel's n runs of
+// hw), one f64 partial per (thread, channel), a fixed shared-memory tree over the
+// 256 threads, then the block's rank-level exchange (finish_exchange).
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(kBnThreads) bn_stats_small_nchw(const ExArgs e, const BnSmallArgs b) {
+  constexpr int VEC = 16 / sizeof(T);
+  extern __shared__ double sm[];  // [256][cpb][2]
+  const int rank = e.rank >= 0 ? e.rank : (int)blockIdx.y;
+  if (rp_aborted(e.t, rank)) return;
+  const int rep = e.rank >= 0 ? 0 : rank;
+  const int cpb = b.cvb, t = threadIdx.x;
+  const int64_t C = b.C, N = b.rows, HW = b.hw;
+  const T* x = (const T*)b.x[rep];
+  const T* dy = BWD ? (const T*)b.dy[rep] : nullptr;
+  const uint32_t seen = state_load(e.t, rank, RP_ST_PH_SEEN + RP_BN_PHASE);
+  const bool vec = (HW % VEC == 0) && ((((uintptr_t)x) & 15u) == 0) && (!BWD || ((((uintptr_t)dy) & 15u) == 0));
+  for (int j = 0; j < cpb; ++j) {
+    const int64_t c = (int64_t)blockIdx.x * cpb + j;
+    double s1 = 0.0, s2 = 0.0;
+    if (c < C) {
+      const float mu = BWD ? b.mean[rep][c] : 0.0f;
+      if (vec) {
+        const int64_t vpr = HW / VEC;  // vectors per (n, c) run
+        for (int64_t q = t; q < N * vpr; q += kBnThreads) {
+          const int64_t n = q / vpr, i = q - n * vpr;
+          const int64_t off = (n * C + c) * HW + i * VEC;
+          Pack16<T> px, pd;
+          px.u = ld128_stream(x + off);
+          if (BWD) pd.u = ld128_stream(dy + off);
+          float f1 = 0.0f, f2 = 0.0f;  // one 16-byte vector in f32, then into f64
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            const float xk = to_acc(px.e[k]);
+            if (BWD) {
+              const float dk = to_acc(pd.e[k]);
+              f1 += dk;
+              f2 = fmaf(dk, xk - mu, f2);
+            } else {
+              f1 += xk;
+              f2 = fmaf(xk, xk, f2);
+            }
+          }
+          s1 += (double)f1;
+          s2 += (double)f2;
+        }
+      } else {
+        for (int64_t q = t; q < N * HW; q += kBnThreads) {
+          const int64_t n = q / HW, i = q - n * HW;
+          const int64_t off = (n * C + c) * HW + i;
+          const double xk = ld_as_f64(x + off);
+          if (BWD) {
+            const double dk = ld_as_f64(dy + off);
+            s1 += dk;
+            s2 = fma(dk, xk - (double)mu, s2);
+          } else {
+            s1 += xk;
+            s2 = fma(xk, xk, s2);
+          }
+        }
+      }
+    }
+    sm[((size_t)t * cpb + j) * 2] = s1;
+    sm[((size_t)t * cpb + j) * 2 + 1] = s2;
+  }
+  __syncthreads();
+  for (int h = kBnThreads >> 1; h > 0; h >>= 1) {  // fixed-order tree over the threads
+    if (t < h) {
+      for (int j = 0; j < cpb; ++j) {
+        sm[((size_t)t * cpb + j) * 2] += sm[((size_t)(t + h) * cpb + j) * 2];
+        sm[((size_t)t * cpb + j) * 2 + 1] += sm[((size_t)(t + h) * cpb + j) * 2 + 1];
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t c = (int64_t)blockIdx.x * cpb + t;
+  const bool owner = t < cpb && c < C;
+  const double v1 = owner ? sm[(size_t)t * 2] : 0.0, v2 = owner ? sm[(size_t)t * 2 + 1] : 0.0;
   finish_exchange(e, rank, blockIdx.x, gridDim.x, seen, c, owner, v1, v2);
 }
 
@@ -892,6 +973,16 @@ const void* small_kernel(bool bwd, int dtype) {
   return nullptr;  // f64: the split path
 }
 
+const void* small_nchw_kernel(bool bwd, int dtype) {
+#define RP_S(DT, T) \
+  if (dtype == DT) return bwd ? (const void*)bn_stats_small_nchw<T, true> : (const void*)bn_stats_small_nchw<T, false>;
+  RP_S(RP_F32, float)
+  RP_S(RP_BF16, __nv_bfloat16)
+  RP_S(RP_F16, __half)
+#undef RP_S
+  return nullptr;
+}
+
 int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, int64_t rows, int64_t ch, int64_t hw,
               int layout, float eps, const float* mean, float* o0, float* o1, float* o2, float* o3, double* count,
               cudaStream_t stream) {
@@ -951,11 +1042,41 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
         }
         b.rows = rows;
         b.C = ch;
+        b.hw = 1;
         b.cvb = cvb;
         ExArgs e;
         fill_ex(c, bwd, eps, rows, hw, ch, o0, o1, o2, o3, count, e);
         void* args[] = {&e, &b};
         return rp_launch(c, sf, dim3((unsigned)blocks, nrep), dim3(kBnThreads), args, ssm, stream);
+      }
+    }
+    const void* nf = small_nchw_kernel(bwd, dtype);
+    if (layout == RP_LAYOUT_NCHW && nf && rows > 0 && !(se && se[0] == '0')) {
+      int occ = 0;
+      const size_t ssm8 = (size_t)kBnThreads * 8 * 2 * sizeof(double);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nf, kBnThreads, ssm8) != cudaSuccess || occ < 1) occ = 1;
+      const int64_t wave = rp_wave_per_rank(c, occ);
+      int cpb = 1;  // channels per block: the fewest that fit one co-resident wave
+      while (cpb < 8 && (ch + cpb - 1) / cpb > wave) cpb *= 2;
+      const int64_t blocks = (ch + cpb - 1) / cpb;
+      // bounded work per thread: <= 256 elements over the block's channels
+      if (blocks <= wave && rows * hw * cpb <= (int64_t)256 * kBnThreads) {
+        BnSmallArgs b;
+        memset(&b, 0, sizeof(b));
+        for (int i = 0; i < nrep; ++i) {
+          b.x[i] = a.x[i];
+          b.dy[i] = a.dy[i];
+          b.mean[i] = a.mean[i];
+        }
+        b.rows = rows;
+        b.C = ch;
+        b.hw = hw;
+        b.cvb = cpb;
+        ExArgs e;
+        fill_ex(c, bwd, eps, rows, hw, ch, o0, o1, o2, o3, count, e);
+        void* args[] = {&e, &b};
+        const size_t ssm = (size_t)kBnThreads * cpb * 2 * sizeof(double);
+        return rp_launch(c, nf, dim3((unsigned)blocks, nrep), dim3(kBnThreads), args, ssm, stream);
       }
     }
   }
