@@ -78,6 +78,15 @@ def test_c_abi_rejects_bad_arguments_without_a_gpu():
     assert lib.rp_all_reduce(None, None, None, 1, 0, 0, 0, 0, 0, None) == 1            # NULL comm
     assert lib.rp_comm_set_block_cap(None, 32) == 1                                     # NULL comm
     assert lib.rp_broadcast(None, None, None, 16, 0, 4, None) == 1                      # relay, NULL comm
+    # round-2 entry points validate before touching a device
+    n = ctypes.c_size_t(0)
+    assert lib.rp_register_export(None, None, 0, None, ctypes.byref(n)) == 1
+    assert lib.rp_register_import(None, None, 0, None) == 1
+    assert lib.rp_unregister(None, 0) == 1
+    assert lib.rp_comm_set_loopback(None, 1) == 1
+    assert lib.rp_comm_topology(None, None, None) == 1
+    assert lib.rp_all_reduce_plan(None, None, None, 1, 0, 0, 0, 0, 0, None) == 1
+    assert lib.rp_register_export_size() > 64
 
 
 # --- virtual-replica rendezvous ------------------------------------------------
