@@ -143,7 +143,12 @@ class _Base:
         device order pairs the same calls on every rank."""
         cur = torch.cuda.current_stream(self.device)
         last = self._last_stream
-        if last is not None and last != cur:
+        # A stream being captured into a CUDA graph may not wait on work outside the
+        # capture (cudaErrorStreamCaptureIsolation): inside a capture the graph's own
+        # stream order sequences its collectives, and replaying a graph while an eager
+        # collective of the same communicator runs on another stream is the caller's
+        # ordering to provide (as for any two streams).
+        if last is not None and last != cur and not torch.cuda.is_current_stream_capturing():
             cur.wait_stream(last)
         self._last_stream = cur
         return cur.cuda_stream
