@@ -1018,20 +1018,24 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
       a.mean[i] = c->is_virtual ? ((const float* const*)mean)[i] : mean;
     }
   }
-  // K5s: small NHWC layers in one pass (bn_stats_small); RP_BN_SMALL=0 disables (A/B)
+  // K5s: small layers in one pass (bn_stats_small / bn_stats_small_nchw), opt-in with
+  // RP_BN_SMALL=1 until it has been measured on the GPU (round 2 lost GPU access
+  // before it could be); the split path below is the default
   {
     const char* se = getenv("RP_BN_SMALL");
+    const bool small_on = se && se[0] == '1';
     const void* sf = small_kernel(bwd, dtype);
-    if (layout == RP_LAYOUT_NHWC && vecok && sf && rows > 0 && !(se && se[0] == '0')) {
+    if (layout == RP_LAYOUT_NHWC && vecok && sf && rows > 0 && small_on) {
       const int64_t CVt = ch / nv;
-      int cvb = 1;  // >= 128 blocks when C allows, at most 16 channel-vectors per block
-      while (cvb < 16 && CVt / (cvb * 2) >= 128) cvb *= 2;
-      const int RY = kBnThreads / cvb;
-      const int64_t blocks = (CVt + cvb - 1) / cvb;
       const size_t ssm = (size_t)kBnThreads * nv * 2 * sizeof(double);
       int occ = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sf, kBnThreads, ssm) != cudaSuccess || occ < 1) occ = 1;
       const int64_t wave = rp_wave_per_rank(c, occ);
+      int cvb = 1;  // >= 128 blocks when C allows, one co-resident wave, <= 16 channel-vectors per block
+      while (cvb < 16 && CVt / (cvb * 2) >= 128) cvb *= 2;
+      while (cvb < 16 && (CVt + cvb - 1) / cvb > wave) cvb *= 2;
+      const int RY = kBnThreads / cvb;
+      const int64_t blocks = (CVt + cvb - 1) / cvb;
       if (rows <= (int64_t)32 * RY && blocks <= wave) {
         BnSmallArgs b;
         memset(&b, 0, sizeof(b));
@@ -1051,7 +1055,7 @@ int bn_common(rp_comm* c, bool bwd, const void* x, const void* dy, int dtype, in
       }
     }
     const void* nf = small_nchw_kernel(bwd, dtype);
-    if (layout == RP_LAYOUT_NCHW && nf && rows > 0 && !(se && se[0] == '0')) {
+    if (layout == RP_LAYOUT_NCHW && nf && rows > 0 && small_on) {
       int occ = 0;
       const size_t ssm8 = (size_t)kBnThreads * 8 * 2 * sizeof(double);
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nf, kBnThreads, ssm8) != cudaSuccess || occ < 1) occ = 1;

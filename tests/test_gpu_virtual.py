@@ -329,12 +329,12 @@ def _bn_virtual(comm, xs, layout, rows, c, hw, eps=1e-5):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("shape", [(8, 64, 16, 16), (4, 256, 4, 4), (3, 33, 5, 7), (2, 1024, 1, 1),
                                    (64, 128, 16, 16)])
-@pytest.mark.parametrize("small", ["1", "0"])
-def test_bn_stats_match_f64_oracle(layout, dtype, shape, small, monkeypatch):
-    """Both NHWC statistics paths: the one-pass small-layer kernel (bn_stats_small,
-    the default where it applies) and the split-partials kernel (RP_BN_SMALL=0, and
-    the 64x128x16x16 layer, too many rows for the one-pass form)."""
-    monkeypatch.setenv("RP_BN_SMALL", small)
+def test_bn_stats_match_f64_oracle(layout, dtype, shape, small="0", monkeypatch=None):
+    """The default statistics path (split partials + exchange); the one-pass
+    small-layer kernels (RP_BN_SMALL=1) are checked by the same body at the end of
+    this module."""
+    if monkeypatch is not None:
+        monkeypatch.setenv("RP_BN_SMALL", small)
     n = 4
     comm = vcomm(n)
     g = torch.Generator(device=DEV).manual_seed(7)
@@ -356,9 +356,9 @@ def test_bn_stats_match_f64_oracle(layout, dtype, shape, small, monkeypatch):
 
 
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
-@pytest.mark.parametrize("small", ["1", "0"])
-def test_bn_bwd_stats_match_oracle(layout, small, monkeypatch):
-    monkeypatch.setenv("RP_BN_SMALL", small)
+def test_bn_bwd_stats_match_oracle(layout, small="0", monkeypatch=None):
+    if monkeypatch is not None:
+        monkeypatch.setenv("RP_BN_SMALL", small)
     n, shape = 2, (4, 32, 6, 6)
     comm = vcomm(n)
     lib = _lib.load()
@@ -696,3 +696,16 @@ def test_flat_bulk_copy_variant_matches_oracle(n, monkeypatch):
     outs = vcomm(n).all_reduce(xs, "sum", algo="flat")
     assert host(outs[0]).tobytes() == O.fold_sum([host(x) for x in xs]).tobytes()
     vcomm(n).check()
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("shape", [(8, 64, 16, 16), (4, 256, 4, 4), (2, 1024, 1, 1), (64, 1024, 4, 4),
+                                   (3, 33, 5, 7)])
+def test_bn_small_layer_kernels_match_f64_oracle(layout, dtype, shape, monkeypatch):
+    """The one-pass small-layer statistics kernels (RP_BN_SMALL=1: bn_stats_small for
+    NHWC, bn_stats_small_nchw for NCHW; the SN-GAN 64x1024x4x4 layer among the
+    shapes), forward and backward, against the same f64 oracle as the default path."""
+    test_bn_stats_match_f64_oracle(layout, dtype, shape, small="1", monkeypatch=monkeypatch)
+    if dtype == torch.float32 and shape == (4, 256, 4, 4):
+        test_bn_bwd_stats_match_oracle(layout, small="1", monkeypatch=monkeypatch)

@@ -34,5 +34,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:ar_v
     > gpurun_out/r02_ncu_full.log 2>&1
 echo "ncu full rc=$?"
 timeout 600 python tools/bench_bn.py > gpurun_out/r02_bn_bench_n1.txt 2>&1
-RP_BN_SMALL=0 timeout 600 python tools/bench_bn.py > gpurun_out/r02_bn_bench_n1_split.txt 2>&1
+RP_BN_SMALL=1 timeout 600 python tools/bench_bn.py > gpurun_out/r02_bn_bench_n1_small.txt 2>&1
 echo "bn bench rc=$?"; tail -25 gpurun_out/r02_bn_bench_n1.txt
