@@ -88,7 +88,7 @@ def _cached(key, fn):
             return _CACHE[key]
     val = fn()
     with _CACHE_LOCK:
-        if len(_CACHE) > 64:
+        if len(_CACHE) > 24:
             _CACHE.clear()
         return _CACHE.setdefault(key, val)
 
